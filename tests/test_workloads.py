@@ -1,0 +1,51 @@
+"""The seeded input generators (workloads/): determinism, shapes, ranges, moments."""
+import math
+
+import numpy as np
+
+import workloads as W
+
+
+def _check_batch(b):
+    assert b.offset[0] == 0 and b.offset[-1] == b.n_req
+    assert (np.diff(b.offset) >= 0).all()
+    assert b.req.dtype == np.int32 and b.req.flags.c_contiguous
+    for k in range(min(b.n_inst, 50)):
+        req, M = b.instance(k)
+        if len(req):
+            assert (np.diff(req[:, 0]) >= 0).all()
+            assert (req[:, 1] >= 1).all() and (req[:, 2] >= 1).all()
+            assert (req[:, 1] + req[:, 3] <= M).all()
+
+
+def test_deterministic():
+    for f in (lambda: W.c1(10, 3, "b"), lambda: W.am1(3, 4), lambda: W.am2(100, 5),
+              lambda: W.c4(2, 6)):
+        assert f().sha256() == f().sha256()
+    assert W.am2(100, 5).sha256() != W.am2(100, 6).sha256()
+
+
+def test_shapes_and_ranges():
+    for b in (W.c1(20, 1, "a"), W.c1(20, 1, "b"), W.am1(4, 2), W.am2(500, 3), W.c4(2, 4),
+              W.random_small(50, 5), W.am1_paper(5, 6)):
+        _check_batch(b)
+    b = W.am2(2500, 7)
+    assert set(np.unique(b.mem)) == set(W.C5_MS)
+    assert b.req[:, 0].min() >= 1 and b.req[:, 0].max() <= 60      # rounds 1..T
+    assert b.req[:, 1].max() <= 5
+    b = W.am1(2, 2)
+    assert (b.req[:, 0] == 0).all() and b.max_requests() == 1000 and (b.mem == 40).all()
+
+
+def test_trace_moments():
+    """Lognormal fit to the published medians/means: the medians are exact by
+    construction; the means come out near 40.62 / 85.32 (truncation by s+o <= M)."""
+    b = W.c3(2, 3)
+    s, o = b.req[:, 1], b.req[:, 2]
+    assert abs(np.median(s) - 11) <= 1 and abs(np.median(o) - 45) <= 2
+    assert abs(s.mean() - 40.62) / 40.62 < 0.15 and abs(o.mean() - 85.32) / 85.32 < 0.1
+    assert (b.mem == 16492).all() and b.max_requests() == 10_000
+    # Poisson(2) per round -> about n/2 rounds of arrivals
+    span = b.instance(0)[0][-1, 0]
+    assert abs(span - 5000) < 400
+    assert abs(math.sqrt(2 * math.log(40.62 / 11)) - 1.616) < 1e-3
