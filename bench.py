@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- MC-SF scheduling rounds/sec over batched instances on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kvsched|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+A step is one pass of the whole hot path over one batch: sched_run_instances (MC-SF,
+Algorithm 1 of arXiv 2502.07115) over every instance of this rank's shard, plus (N > 1) the
+NCCL all_gather of per-instance (TEL, rounds, status) and the all_reduce of totals that the
+north star names.  Workload (default) = BASELINE config 5: the Arrival-Model-2 sweep
+lambda x M x seed (10^6 instances per GPU; weak scaling: every rank runs its own 10^6).
+Inputs are device-resident before timing and larger than L2 (800 MB vs 126 MB).
+
+The JSON line carries the device-timed value, the end-to-end value through the C ABI with
+host buffers, the HBM roofline of the simulation kernel, the CPU oracle baseline, clocks
+and the kernel launch count.  --impl reference times the oracle (the CPU reference) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import workloads as W  # noqa: E402
+
+METRIC = "MC-SF scheduling rounds/sec over batched instances"
+UNIT = "rounds/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kvsched", choices=["kvsched", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4", "c3"])
+    ap.add_argument("--instances", type=int, default=0, help="instances per GPU (0 = config size)")
+    ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def make_workload(name: str, n: int, rank: int):
+    if name == "c5":
+        n = n or 1_000_000
+        return W.am2(n, seed=5, id0=rank * n), dict(workload="C5 AM2 sweep lambda{0.5..1.5} x M{30..50}",
+                                                    instances_per_gpu=n, requests_per_instance="Poisson(lambda T), T~U{40..60}")
+    if name == "c2":
+        n = n or 10_000
+        return W.am1(n, seed=2 + 1000 * rank), dict(workload="C2 AM1 n=1000 at t=0, M=40",
+                                                    instances_per_gpu=n, requests_per_instance=1000)
+    if name == "c4":
+        n = n or 20_000
+        return W.c4(n, seed=4 + 1000 * rank), dict(workload="C4 trace-shaped n=1000 lambda=2/round M=16492",
+                                                   instances_per_gpu=n, requests_per_instance=1000)
+    n = n or 512
+    return W.c3(n, seed=3 + 1000 * rank), dict(workload="C3 trace-shaped n=10^4 lambda=2/round M=16492",
+                                               instances_per_gpu=n, requests_per_instance=10_000)
+
+
+def policy_of(K, name):
+    if name == "alpha":
+        return K.Policy("alpha", (3, 10))
+    if name == "alpha_beta":
+        return K.Policy("alpha_beta", (1, 5), W.beta_threshold(0.1), seed=1)
+    return K.Policy(name)
+
+
+def oracle_policy(name):
+    import oracle
+    return {"mcsf": (oracle.MCSF, {}), "mcbench": (oracle.MCBENCH, {}),
+            "alpha": (oracle.ALPHA, dict(alpha=(3, 10))),
+            "alpha_beta": (oracle.ALPHA_BETA, dict(alpha=(1, 5), beta_thresh=W.beta_threshold(0.1), seed=1))}[name]
+
+
+def cpu_oracle_rate(batch, policy: str, seconds: float, gid0: int = 0):
+    """The oracle as it stands, on all host cores, over a bounded prefix of the workload."""
+    import oracle
+    pol, kw = oracle_policy(policy)
+    nthreads = os.cpu_count() or 1
+    chunk = max(1, min(batch.n_inst, 2000))
+    rounds = 0
+    insts = 0
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < seconds and k < batch.n_inst:
+        sub = batch.subset(range(k, min(k + chunk, batch.n_inst)))
+        out = oracle.simulate_batch(sub.offset, sub.req, sub.mem, pol, gid0=gid0 + k, nthreads=nthreads, **kw)
+        rounds += int(out["rounds"][out["status"] == 0].sum())
+        insts += sub.n_inst
+        k += chunk
+    dt = time.perf_counter() - t0
+    return dict(value=rounds / dt, unit=UNIT, cores=nthreads, kind="oracle",
+                sample=f"first {insts} instances of the same workload ({rounds} rounds, {dt:.1f} s)",
+                instances_per_s=insts / dt)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(f"/tmp/kvsched_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        self.path.unlink(missing_ok=True)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def algorithmic_bytes(batch, fields) -> int:
+    """HBM bytes the method must move per launch: request tuples, offsets and budgets in;
+    the requested outputs out (DESIGN "Roofline")."""
+    b = batch.n_req * 16 + (batch.n_inst + 1) * 8 + batch.n_inst * 4
+    for k in fields:
+        if k in ("completion", "start"):
+            b += batch.n_req * 4
+        elif k in ("tel", "rounds", "decision_rounds", "evictions"):
+            b += batch.n_inst * 8
+        else:
+            b += batch.n_inst * 4
+    return b
+
+
+def ncu_traffic(kernel_name: str):
+    """dram bytes per launch from the committed ncu capture (profiles/), if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get("kernels", {}).get(kernel_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    batch, cfg = make_workload(args.workload, args.instances, 0)
+    per_step = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
+    for _ in range(args.warmup):
+        cpu_oracle_rate(batch, args.policy, per_step)
+    vals = [cpu_oracle_rate(batch, args.policy, per_step) for _ in range(args.steps)]
+    v = statistics.median([x["value"] for x in vals])
+    cfg.update(policy=args.policy, l2="n/a (CPU)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "oracle",
+                             "sample": vals[0]["sample"] + " per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_07115_b200 as K
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    batch, cfg = make_workload(args.workload, args.instances, rank)
+    hints = K.hints_of(batch)
+    off, req, mem = K.to_device(batch, dev)
+    fields = K.kvsched.OUT_FIELDS
+    out = K.alloc_outputs(batch.n_inst, batch.n_req, dev, fields)
+    stream = torch.cuda.current_stream(dev)
+    ctx = K.Context(local, stream=stream.cuda_stream)
+    pol = policy_of(K, args.policy)
+    id0 = rank * batch.n_inst
+    if world > 1:
+        gathered = torch.empty((world, 3, batch.n_inst), dtype=torch.int64, device=dev)
+        mine = torch.empty((3, batch.n_inst), dtype=torch.int64, device=dev)
+        totals = torch.empty(4, dtype=torch.int64, device=dev)
+
+    def step():
+        ctx.run(off, req, mem, pol, out, id0=id0, hints=hints)
+        if world > 1:
+            # the north star's only collective: gather per-instance (TEL, rounds, status) and
+            # reduce the totals over NVLink (NCCL)
+            mine[0].copy_(out["tel"][:batch.n_inst])
+            mine[1].copy_(out["rounds"][:batch.n_inst])
+            mine[2].copy_(out["status"][:batch.n_inst])
+            dist.all_gather_into_tensor(gathered, mine)
+            totals[0] = out["tel"][:batch.n_inst].clamp(min=0).sum()
+            totals[1] = out["rounds"][:batch.n_inst].clamp(min=0).sum()
+            totals[2] = (out["status"][:batch.n_inst] == 0).sum()
+            totals[3] = batch.n_inst
+            dist.all_reduce(totals)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    rounds_rank = int(out["rounds"][:batch.n_inst].clamp(min=0).sum().item())
+    ok_rank = int((out["status"][:batch.n_inst] == 0).sum().item())
+
+    clocks = Clocks(local)
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ctx.set_timing(False)
+    st = ctx.stats()
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([rounds_rank, ok_rank, batch.n_inst], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot)
+    ms_max = float(t_max.item())
+    rounds_all, ok_all, inst_all = (int(x) for x in tot.tolist())
+    value = rounds_all * args.steps / (ms_max / 1000.0)
+
+    # roofline of the simulation kernel: algorithmic bytes per launch / mean launch time
+    kname = ctx.last_kernel()
+    k_ms = st["sim_kernel_ms"] / max(st["sim_kernel_launches"], 1)
+    alg = algorithmic_bytes(batch, fields)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak_gbs = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg / (k_ms / 1000.0) / 1e9
+    traffic = ncu_traffic(kname)
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+            "frac": achieved / peak_gbs, "traffic": traffic, "alg_bytes_per_launch": alg,
+            "kernel_ms": k_ms, "peak_source": "measured" if peaks else "fallback",
+            "kernel_share_of_step": (st["sim_kernel_ms"] / args.steps) / (ms_max / args.steps) if args.steps else None}
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e and world >= 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_off, h_req, h_mem = pin(batch.offset), pin(batch.req), pin(batch.mem)
+        h_out = {}
+        for k in fields:
+            n = batch.n_req if k in ("completion", "start") else batch.n_inst
+            dt = torch.int64 if k in K.kvsched.OUT_I64 else torch.int32
+            h_out[k] = torch.empty(max(n, 1), dtype=dt).pin_memory()
+        host = {k: v.numpy() for k, v in h_out.items()}
+        a_off, a_req, a_mem = h_off.numpy(), h_req.numpy(), h_mem.numpy()
+        ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints)      # warm
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        same = np.array_equal(host["rounds"][:batch.n_inst], out["rounds"][:batch.n_inst].cpu().numpy())
+        h2d = batch.n_req * 16 + (batch.n_inst + 1) * 8 + batch.n_inst * 4
+        d2h = algorithmic_bytes(batch, fields) - h2d
+        e2e = {"value": rounds_all * args.e2e_steps / (e_ms / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "ms_per_step": e_ms / args.e2e_steps, "matches_device_run": bool(same)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_rate(batch, args.policy, args.cpu_seconds, gid0=id0)
+
+    if rank == 0:
+        cfg.update(policy=args.policy, l2="inputs %.0f MB > 126 MB L2 (no flush needed)" % (batch.req.nbytes / 1e6),
+                   parallelism=f"instance-sharded x{world}", instances_total=inst_all,
+                   instances_ok=ok_all, rounds_per_step=rounds_all,
+                   generator=W.GENERATOR_VERSION)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": cfg, "instances_per_s": inst_all * args.steps / (ms_max / 1000.0),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
+                "gpu_launches": st["launches"]}
+        print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

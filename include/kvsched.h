@@ -1,0 +1,179 @@
+/*
+ * kvsched.h -- C ABI of libkvsched.so, the B200 (sm_100a) batched simulator of the online
+ * batch scheduler of arXiv 2502.07115 ("Online Scheduling for LLM Inference with KV Cache
+ * Constraints") and its baseline policies.
+ *
+ * Citations "P:<n>" are lines of the paper's LaTeX source.  Where the paper is
+ * silent the reading adopted is named "DESIGN Qn" and listed in DESIGN.md.
+ *
+ * The model.  One worker with KV budget M.  Request i arrives at round a_i with a
+ * prompt of s_i tokens and an output of o_i tokens (the scheduler sees a prediction o~_i,
+ * P:91).  Started at round p_i it is processed for o_i consecutive unit rounds,
+ * holding s_i + k KV slots at round p_i + k for k = 1..o_i (Eq. 3), and completes at
+ * c_i = p_i + o_i.  TEL = sum_i (c_i - a_i).
+ *
+ * Policies.
+ *   SCHED_MCSF        Algorithm 1: each round sort the waiting queue by o~
+ *                     (ties by arrival position, DESIGN Q5) and admit the longest prefix for
+ *                     which Eq. 5 holds at every future round.
+ *   SCHED_MC_BENCH    Algorithm 2: the same test in arrival order, projected
+ *                     with the true o.
+ *   SCHED_ALPHA       alpha-protection greedy: FCFS admission while the next-
+ *                     round occupancy plus s_i+1 stays <= floor((1-alpha)M); when the batch
+ *                     of a round needs more than M, every active request is cleared.
+ *   SCHED_ALPHA_BETA  alpha-protection beta-clearing: on overflow each active request
+ *                     is cleared with probability beta, in whole passes until the batch fits
+ *                     (DESIGN Q14); draws are Philox4x32-10 on (t, pass, idx, 0) keyed by
+ *                     seed ^ (gid * 0x9E3779B97F4A7C15).
+ *
+ * Conventions for every entry point.
+ *   - Integers only cross the boundary.  All sizes are in KV slots (tokens) and rounds.
+ *   - Unless a function says "host", every pointer is a CUDA device pointer on the context's
+ *     device, caller-owned; the library never retains or frees caller memory.
+ *   - Work is enqueued asynchronously on the context's stream; nothing synchronises the host
+ *     unless stated (sched_run_instances synchronises only when a size hint is 0).
+ *   - Argument errors are detected synchronously, nothing is enqueued, a negative SCHED_E_*
+ *     is returned and sched_last_error() describes it.  Per-instance data problems never
+ *     fail the call: they set that instance's status (SCHED_INST_*).
+ *   - Outputs are a pure function of (inputs, policy, instance_id0): they do not depend on
+ *     the grid shape, the number of GPUs or the order instances are processed in.
+ */
+#ifndef KVSCHED_H
+#define KVSCHED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVSCHED_ABI_VERSION 1
+
+/* return codes */
+enum {
+    SCHED_OK = 0,
+    SCHED_E_ARG = -1,      /* bad argument (null pointer, n < 0, unknown policy, alpha out of
+                              [0,1), misaligned req, size limits exceeded)              */
+    SCHED_E_CUDA = -2,     /* a CUDA runtime call or kernel launch failed                 */
+    SCHED_E_NOMEM = -3,    /* scratch allocation failed                                   */
+    SCHED_E_STATE = -4     /* bad context                                                 */
+};
+
+/* policies (see above) */
+enum { SCHED_MCSF = 0, SCHED_MC_BENCH = 1, SCHED_ALPHA = 2, SCHED_ALPHA_BETA = 3 };
+
+/* per-instance status */
+enum {
+    SCHED_INST_OK = 0,
+    SCHED_INST_INVALID = 1,    /* data error: a not sorted, a < 0, s/o/o~ < 1; MC-SF: s+o~ > M
+                                  or o~ < o; other policies: s+o > M (DESIGN Q8)          */
+    SCHED_INST_LIVELOCK = 2,   /* round cap passed, or alpha head-of-line blocked for ever   */
+    SCHED_INST_UNSUPPORTED = 3 /* instance exceeds the caller's size hints / kernel limits  */
+};
+
+/* Limits of this build (sched_run_instances returns SCHED_E_ARG beyond them). */
+#define SCHED_MAX_REQUESTS_PER_INSTANCE 32768
+#define SCHED_MAX_LEN 32767     /* max over requests of max(o, o~), also bounds M - 1 use */
+
+typedef struct sched_ctx sched_ctx;   /* opaque: device, stream, scratch, timers */
+
+/* A batch of independent instances in CSR form.                                        */
+typedef struct {
+    int64_t n_instances;        /* >= 0                                                     */
+    const int64_t *req_offset;  /* [n_instances+1]; offset[0] = 0, non-decreasing; the
+                                   requests of instance k are rows offset[k]..offset[k+1]-1 */
+    const int32_t *req;         /* [n_req][4] rows {a_i, s_i, o_i, o~_i}, 16-byte aligned;
+                                   rows of an instance sorted by a (non-decreasing); the row
+                                   position inside the instance is the request id idx and
+                                   the tie-break of every order (DESIGN Q5)                  */
+    const int32_t *mem_limit;   /* [n_instances] budget M of each instance           */
+    int64_t instance_id0;       /* global id of instance 0 (shards; alpha-beta RNG key gid)  */
+    int32_t max_requests;       /* upper bound on requests per instance, or 0 = measure      */
+    int32_t max_mem;            /* upper bound on M, or 0 = measure                          */
+    int32_t max_len;            /* upper bound on max(o_i, o~_i), or 0 = measure             */
+    int32_t reserved;           /* must be 0                                                 */
+} sched_instances;
+/* "measure" runs a reduction kernel and synchronises the stream to read the bounds.
+ * Instances that exceed a caller-given bound get status SCHED_INST_UNSUPPORTED.            */
+
+typedef struct {
+    int32_t policy;             /* SCHED_MCSF .. SCHED_ALPHA_BETA                            */
+    int32_t alpha_num;          /* alpha = alpha_num / alpha_den in [0, 1) (alpha policies);  */
+    int32_t alpha_den;          /*   budget B = ((den - num) * M) / den (DESIGN Q15)         */
+    int32_t reserved;           /* must be 0                                                 */
+    uint64_t beta_thresh;       /* alpha-beta: evict iff u32 draw < beta_thresh, in [0, 2^32];
+                                   round(beta * 2^32); 2^32 = always (beta = 1)              */
+    uint64_t seed;              /* alpha-beta RNG key                                        */
+    int64_t round_cap;          /* > 0: absolute round after which the run is LIVELOCK;
+                                   <= 0: min(2^30, 16 (max_a + sum_i o_i) + 64) (DESIGN Q23)  */
+} sched_policy;
+
+/* Outputs; every pointer may be NULL (= not requested).                                 */
+typedef struct {
+    int32_t *completion;        /* [n_req] c_i of the last admission not later evicted, else -1 */
+    int32_t *start;             /* [n_req] p_i likewise, else -1                            */
+    int64_t *tel;               /* [n_instances] sum_i (c_i - a_i); -1 unless OK      */
+    int64_t *rounds;            /* [n_instances] |union_i [a_i, c_i)| (DESIGN Q11); -1 unless OK */
+    int64_t *decision_rounds;   /* [n_instances] rounds whose waiting queue was non-empty     */
+    int64_t *evictions;         /* [n_instances] requests cleared (alpha policies)           */
+    int32_t *makespan;          /* [n_instances] max_i c_i; -1 unless OK                     */
+    int32_t *peak_mem;          /* [n_instances] max over processed rounds of the batch's KV
+                                   occupancy sum (s_j + t+1 - p_j) (Eq. 3 at t+1)            */
+    int32_t *status;            /* [n_instances] SCHED_INST_*                                */
+} sched_outputs;
+
+/* Create a context on `device` that enqueues on `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  *out receives the context.                                    */
+int sched_init(sched_ctx **out, int device, void *cuda_stream);
+
+/* Change the stream later calls enqueue on.                                               */
+int sched_set_stream(sched_ctx *ctx, void *cuda_stream);
+
+/* Simulate every instance of `inst` under `pol` (device pointers).  One warp per instance
+ * on a persistent grid; MC policies with M <= 64 take the fused register-profile kernel,
+ * everything else the shared-memory ring kernel (DESIGN "Kernels").                       */
+int sched_run_instances(sched_ctx *ctx, const sched_instances *inst, const sched_policy *pol,
+                        const sched_outputs *out);
+
+/* Same, with HOST pointers in `inst` and `out` (pinned memory recommended): copies inputs to
+ * context-owned device buffers, runs, copies the requested outputs back and synchronises
+ * the stream before returning.                                                           */
+int sched_run_instances_host(sched_ctx *ctx, const sched_instances *inst,
+                             const sched_policy *pol, const sched_outputs *out);
+
+/* TEL of every instance from a completion array (device): tel[k] = sum_i (c_i - a_i) over
+ * instance k, or -1 if some c_i < 0; *tel_total = sum of the non-negative tel[k].  Either
+ * output may be NULL.  Only inst->n_instances, req_offset and req are read.               */
+int sched_latency(sched_ctx *ctx, const sched_instances *inst, const int32_t *completion,
+                  int64_t *tel, int64_t *tel_total);
+
+/* The counter-based RNG of the alpha-beta policy, exposed for known-answer tests:
+ * out[4i..4i+3] = Philox4x32-10(counter ctr[4i..4i+3], key key[2i..2i+1]) (Salmon et al.,
+ * SC'11) for i < n.  Device pointers.                                                    */
+int sched_philox4x32_10(sched_ctx *ctx, int64_t n, const uint32_t *ctr, const uint32_t *key,
+                        uint32_t *out);
+
+/* Kernel accounting of this context since the last reset: number of kernel launches the
+ * library made, and the summed device time (ms, CUDA events on the context's stream) of
+ * the simulation kernels when timing is enabled.  Host pointers; either may be NULL.     */
+int sched_set_timing(sched_ctx *ctx, int enable);
+int sched_get_stats(sched_ctx *ctx, int64_t *launches, double *sim_kernel_ms,
+                    int64_t *sim_kernel_launches);
+int sched_reset_stats(sched_ctx *ctx);
+
+/* Name of the simulation kernel the last sched_run_instances call launched (static string). */
+const char *sched_last_kernel(const sched_ctx *ctx);
+
+/* Release the context's scratch and the context.                                         */
+int sched_finalize(sched_ctx *ctx);
+
+/* Text of the last error on this context ("" if none); NULL ctx -> last sched_init error. */
+const char *sched_last_error(const sched_ctx *ctx);
+
+/* ABI version compiled into the library (KVSCHED_ABI_VERSION).                          */
+int sched_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVSCHED_H */

@@ -1,0 +1,417 @@
+// kernel_ring.cuh -- per-instance warp simulator for any budget M (all four policies).
+//
+// Same round structure as kernel_small.cuh, but the memory profile is a ring of L int32
+// slots in shared memory (slot r & (L-1) holds absolute round r, L a power of two larger
+// than every request length), so a candidate's Eq. 5 test and its admission are
+// ceil(w/32) warp-wide passes over its own window.  Per-request data stay in HBM/L2 and
+// are fetched when a request reaches the head of the queue.
+//
+//   MC-SF / MC-Benchmark : ring = projected memory of S (Eq. 5 LHS), as in the small kernel.
+//   alpha / alpha-beta    : ring = actual memory (Eq. 3, true o).  Admission is FCFS with
+//                           threshold B = floor((1-alpha)M) on the next-round occupancy
+//                           (DESIGN Q12); when Mem(t+1) > M the active set is cleared
+//                            or thinned by independent Philox draws (DESIGN Q14).
+//                           The in-flight set is a bitmap over idx (plus start rounds in
+//                           global scratch) walked only on overflow.
+#pragma once
+#include "params.cuh"
+
+namespace kv {
+
+struct RingSmem {
+    int *prof;        // [L]
+    uint32_t *bm;     // [NP/32] waiting queue
+    uint32_t *sm;     // [32]
+    uint32_t *infl;   // [NP/32] in-flight set (alpha policies)
+};
+
+__host__ __device__ inline int ring_warp_bytes(int L, int NP, int policy)
+{
+    int b = L * 4 + (NP / 32) * 4 + 32 * 4;
+    if (policy >= POL_ALPHA) b += (NP / 32) * 4;
+    return (b + 15) & ~15;
+}
+
+// Eq. 5 for one candidate: Prof(t+tau) + s + tau <= M for tau in [1, w]
+__device__ __forceinline__ bool ring_fits(const int *prof, int mask, int t, int s, int w, long long M)
+{
+    const int lane = lane_id();
+    for (int base = 1; base <= w; base += 64) {
+        const int ta = base + lane, tb = base + 32 + lane;
+        const int va = ta <= w ? prof[(t + ta) & mask] : 0;
+        const int vb = tb <= w ? prof[(t + tb) & mask] : 0;
+        const bool bad = (ta <= w && (long long)va + s + ta > M) || (tb <= w && (long long)vb + s + tb > M);
+        if (__any_sync(KV_FULL, bad)) return false;
+    }
+    return true;
+}
+
+// Prof(t+tau) += sign * (base + tau) for tau in [1, e]
+__device__ __forceinline__ void ring_ramp(int *prof, int mask, int t, int e, int base, int sign)
+{
+    for (int tau = lane_id() + 1; tau <= e; tau += 32) prof[(t + tau) & mask] += sign * (base + tau);
+}
+
+// max of Prof(t+tau) over tau in [1, d] and zero tau in [1, z]
+__device__ __forceinline__ int ring_max_zero(int *prof, int mask, int t, int d, int z)
+{
+    int v = 0;
+    const int e = max(d, z);
+    for (int tau = lane_id() + 1; tau <= e; tau += 32) {
+        int *q = &prof[(t + tau) & mask];
+        if (tau <= d) v = max(v, *q);
+        if (tau <= z) *q = 0;
+    }
+    __syncwarp();
+    return warp_max_i32(v);
+}
+
+template <int POL>
+__device__ void ring_instance(const KParams &P, long long inst, const RingSmem &S)
+{
+    constexpr bool MC = POL == POL_MCSF || POL == POL_MCBENCH;
+    const int lane = lane_id();
+    const long long off = P.offset[inst];
+    const int n = (int)(P.offset[inst + 1] - off);
+    const int M = P.mem[inst];
+    const int L = P.L, mask = L - 1;
+    const int *reqi = reinterpret_cast<const int *>(P.req);
+    InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
+
+    // ---- validate (coalesced pass) ------------------------------------------------------
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem;
+    long long suma = 0, sumo = 0;
+    if (!unsup) {
+        for (int k = lane; k < n; k += 32) {
+            const int4 r = P.req[off + k];
+            bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
+            if (k > 0) bad |= reqi[(off + k - 1) * 4] > r.x;
+            if (POL == POL_MCSF) {
+                bad |= (long long)r.y + r.w > M || r.w < r.z;
+                unsup |= r.w != r.z;                 // early completion: small kernel only
+            } else {
+                bad |= (long long)r.y + r.z > M;
+            }
+            unsup |= r.z > P.max_len || (POL == POL_MCSF && r.w > P.max_len);
+            suma += r.x;
+            sumo += r.z;
+        }
+    }
+    bad = __any_sync(KV_FULL, bad);
+    unsup = __any_sync(KV_FULL, unsup);
+    suma = warp_sum_i64(suma);
+    sumo = warp_sum_i64(sumo);
+    if (unsup || bad) {
+        res.status = unsup ? ST_UNSUPPORTED : ST_INVALID;
+        fill_unscheduled(P, off, n);
+        write_result(P, inst, res);
+        return;
+    }
+    if (n == 0) { write_result(P, inst, res); return; }
+
+    const int NPi = next_pow2(max(n, 32));
+    const int nw = NPi >> 5;
+    for (int i = lane; i < L; i += 32) S.prof[i] = 0;
+    for (int w = lane; w < nw; w += 32) {
+        S.bm[w] = 0u;
+        if (!MC) S.infl[w] = 0u;
+    }
+    S.sm[lane] = 0u;
+    __syncwarp();
+    WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
+
+    const long long cap = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
+    const long long B = MC ? 0 : ((long long)(P.alpha_den - P.alpha_num) * M) / P.alpha_den;
+    const unsigned long long gid = P.id0 + (unsigned long long)inst;
+
+    int t = reqi[off * 4];
+    int next = 0, a_next = t;
+    int h = KV_INF;
+    uint4 he = make_uint4(0, 0, 0, 0);   // head entry {s, w, o, idx}
+    bool hstale = false;
+    long long sumc = 0, rounds = 0, drounds = 0, evictions = 0;
+    int maxc = -1, peak = 0, status = ST_OK;
+    int mem_prev = 0;                    // alpha: Mem(t) of the previous round
+
+    auto fetch = [&](int r) -> uint4 {
+        if (POL == POL_MCSF) return P.rq[off + r];
+        const int4 q = P.req[off + r];
+        return make_uint4((uint32_t)q.y, (uint32_t)q.z, (uint32_t)q.z, (uint32_t)r);
+    };
+
+    for (;;) {
+        if (h == KV_INF) {
+            if (MC) {
+                if (a_next == KV_INF) {                        // drain
+                    const long long E = min((long long)maxc, cap + 1);
+                    if (E > t) peak = max(peak, ring_max_zero(S.prof, mask, t, (int)min(E - t, (long long)L), 0));
+                    if (maxc > t) rounds += maxc - t;
+                    if ((long long)maxc >= cap + 1) status = ST_LIVELOCK;
+                    break;
+                }
+                const int tn = a_next;
+                if (tn > t) {                                  // skip rounds t..tn-1
+                    const long long E = min((long long)tn, cap + 1);
+                    const int d = E > t ? (int)min(E - t, (long long)L) : 0;
+                    peak = max(peak, ring_max_zero(S.prof, mask, t, d, min(tn - t, L)));
+                    rounds += max(0, min(tn, maxc) - t);
+                    if (tn > cap) { status = ST_LIVELOCK; break; }
+                    t = tn;
+                }
+            } else if (mem_prev == 0) {                        // R and S empty: idle jump
+                if (a_next == KV_INF) break;
+                t = max(t, a_next);
+            }
+        }
+        if (t > cap) { status = ST_LIVELOCK; break; }
+
+        // arrivals
+        while (a_next <= t) {
+            const int k = next + lane;
+            const int ak = k < n ? reqi[(off + k) * 4] : KV_INF;
+            const bool take = ak <= t;
+            const int cnt = __popc(__ballot_sync(KV_FULL, take));
+            int rk = KV_INF;
+            if (take) {
+                rk = (POL == POL_MCSF) ? P.arank[off + k] : k;
+                q_insert(Q, rk);
+            }
+            const int mn = warp_min_i32(rk);
+            if (mn < h) { h = mn; hstale = true; }
+            next += cnt;
+            a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? reqi[(off + next) * 4] : KV_INF);
+        }
+        __syncwarp();
+
+        const bool had_R = h != KV_INF;
+        if (had_R) ++drounds;
+        if (MC) {
+            if (had_R) {
+                if (hstale) { he = fetch(h); hstale = false; }
+                for (;;) {
+                    const int s = (int)he.x, w = (int)he.y, o = (int)he.z, idx = (int)he.w;
+                    if (!ring_fits(S.prof, mask, t, s, w, M)) break;
+                    ring_ramp(S.prof, mask, t, w, s, +1);
+                    const int c = t + o;
+                    if (lane == 0) {
+                        if (P.completion) P.completion[off + idx] = c;
+                        if (P.start) P.start[off + idx] = t;
+                    }
+                    sumc += c;
+                    maxc = max(maxc, c);
+                    __syncwarp();
+                    h = q_pop_head(Q, h);
+                    if (h == KV_INF) break;
+                    he = fetch(h);
+                }
+            }
+            ++rounds;
+        } else {
+            const int occ = S.prof[(t + 1) & mask];           // Mem(t+1) of S
+            const bool idle_before = occ == 0;
+            long long Lnext = occ;
+            int admitted = 0;
+            if (had_R) {
+                if (hstale) { he = fetch(h); hstale = false; }
+                for (;;) {
+                    const int s = (int)he.x, o = (int)he.z, idx = (int)he.w;
+                    if (Lnext + s + 1 > B) break;                   // (1-alpha)M threshold
+                    Lnext += s + 1;
+                    ring_ramp(S.prof, mask, t, o, s, +1);
+                    const int c = t + o;
+                    if (lane == 0) {
+                        if (P.completion) P.completion[off + idx] = c;
+                        if (P.start) P.start[off + idx] = t;
+                        P.pstart[off + idx] = t;                            // start scratch
+                        S.infl[idx >> 5] |= 1u << (idx & 31);
+                    }
+                    sumc += c;
+                    ++admitted;
+                    __syncwarp();
+                    h = q_pop_head(Q, h);
+                    if (h == KV_INF) break;
+                    he = fetch(h);
+                }
+            }
+            __syncwarp();
+            int mem = S.prof[(t + 1) & mask];
+            if (mem > M) {
+                // overflow of the batch of round t (DESIGN Q13): clear or thin
+                const int *pst = P.pstart;
+                for (int pass = 0;; ++pass) {
+                    int left = 0;
+                    for (int wb = 0; wb < nw; wb += 32) {
+                        const int wi = wb + lane;
+                        uint32_t bits = wi < nw ? S.infl[wi] : 0u;
+                        uint32_t keep = bits;
+                        while (__any_sync(KV_FULL, bits != 0u)) {
+                            int j = -1, pj = 0, sj = 0, oj = 0;
+                            bool ev = false, act = false;
+                            if (bits) {
+                                j = (wi << 5) + __ffs(bits) - 1;
+                                bits &= bits - 1;
+                                pj = pst[off + j];
+                                sj = reqi[(off + j) * 4 + 1];
+                                oj = reqi[(off + j) * 4 + 2];
+                                act = pj + oj > t;
+                                if (!act) keep &= ~(1u << (j & 31));   // completed earlier
+                                else {
+                                    ev = (POL == POL_ALPHA) ||
+                                         (unsigned long long)evict_draw(P.seed, gid, t, pass, j) < P.beta_thresh;
+                                    if (ev) keep &= ~(1u << (j & 31));
+                                }
+                            }
+                            left += __popc(__ballot_sync(KV_FULL, act && !ev));
+                            uint32_t evm = __ballot_sync(KV_FULL, ev);
+                            if (evm) {
+                                evictions += __popc(evm);
+                                sumc -= warp_sum_i64(ev ? (long long)(pj + oj) : 0ll);
+                                const int mn = warp_min_i32(ev ? j : KV_INF);
+                                if (mn < h) { h = mn; hstale = true; }
+                                if (ev) {
+                                    q_insert(Q, j);
+                                    if (P.completion) P.completion[off + j] = -1;
+                                    if (P.start) P.start[off + j] = -1;
+                                }
+                                if (POL == POL_ALPHA_BETA) {
+                                    while (evm) {                       // remove its ramp
+                                        const int l = __ffs(evm) - 1;
+                                        evm &= evm - 1;
+                                        const int s_ = __shfl_sync(KV_FULL, sj, l);
+                                        const int p_ = __shfl_sync(KV_FULL, pj, l);
+                                        const int o_ = __shfl_sync(KV_FULL, oj, l);
+                                        __syncwarp();
+                                        ring_ramp(S.prof, mask, t, p_ + o_ - t, s_ + t - p_, -1);
+                                    }
+                                }
+                            }
+                        }
+                        if (wi < nw) S.infl[wi] = keep;
+                    }
+                    __syncwarp();
+                    if (POL == POL_ALPHA) {
+                        for (int i = lane; i < L; i += 32) S.prof[i] = 0;
+                        __syncwarp();
+                        mem = 0;
+                        break;
+                    }
+                    left = __shfl_sync(KV_FULL, left, 0);
+                    mem = S.prof[(t + 1) & mask];
+                    if (mem <= M || left == 0) break;
+                }
+            }
+            if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
+            if (had_R || !idle_before) ++rounds;
+        }
+        __syncwarp();
+        const int mnow = S.prof[(t + 1) & mask];                   // Mem(t+1) of the batch
+        peak = max(peak, mnow);
+        mem_prev = mnow;
+        __syncwarp();
+        if (lane == 0) S.prof[(t + 1) & mask] = 0;
+        __syncwarp();
+        ++t;
+    }
+
+    if (status != ST_OK) {
+        for (int k = next + lane; k < n; k += 32) {
+            if (P.completion) P.completion[off + k] = -1;
+            if (P.start) P.start[off + k] = -1;
+        }
+        for (int w = lane; w < nw; w += 32) {
+            uint32_t bits = S.bm[w];
+            while (bits) {
+                const int r = (w << 5) + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int idx = (POL == POL_MCSF) ? (int)P.rq[off + r].w : r;
+                if (P.completion) P.completion[off + idx] = -1;
+                if (P.start) P.start[off + idx] = -1;
+            }
+        }
+    }
+    if (!MC) {
+        // makespan of the final schedule
+        int mx = -1;
+        if (status == ST_OK)
+            for (int k = lane; k < n; k += 32) mx = max(mx, P.pstart[off + k] + reqi[(off + k) * 4 + 2]);
+        maxc = warp_max_i32(mx);
+    }
+    res.tel = sumc - suma;
+    res.rounds = rounds;
+    res.decision_rounds = drounds;
+    res.evictions = evictions;
+    res.makespan = maxc;
+    res.peak = peak;
+    res.status = status;
+    write_result(P, inst, res);
+}
+
+template <int POL>
+__global__ void __launch_bounds__(128) k_ring(const KParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *base = smem_raw + (size_t)warp * P.warp_bytes;
+    RingSmem S;
+    S.prof = reinterpret_cast<int *>(base);
+    S.bm = reinterpret_cast<uint32_t *>(base + P.L * 4);
+    S.sm = reinterpret_cast<uint32_t *>(base + P.L * 4 + (P.NP / 32) * 4);
+    S.infl = reinterpret_cast<uint32_t *>(base + P.L * 4 + (P.NP / 32) * 4 + 128);
+
+    long long inst = 0;
+    if (lane == 0) inst = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
+    inst = __shfl_sync(KV_FULL, inst, 0);
+    while (inst < P.n_inst) {
+        long long nxt = 0;
+        if (lane == 0) nxt = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
+        ring_instance<POL>(P, inst, S);
+        inst = __shfl_sync(KV_FULL, nxt, 0);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// MC-SF rank prepass for the ring kernel: one CTA per instance sorts (o~, idx) keys in
+// shared memory (bitonic) and writes per-rank entries {s, o~, o, idx} and rank[idx].
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_rank_sort(const KParams P, uint4 *rq, int *arank)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t *keys = reinterpret_cast<uint32_t *>(smem_raw);
+    for (long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {
+        const long long off = P.offset[inst];
+        const int n = (int)(P.offset[inst + 1] - off);
+        if (n <= 0 || n > P.max_requests) continue;
+        const int NPi = next_pow2(n);
+        for (int k = threadIdx.x; k < NPi; k += blockDim.x) {
+            uint32_t key = 0xffffffffu;
+            if (k < n) {
+                const uint32_t w = (uint32_t)min(max(P.req[off + k].w, 0), 0x1ffff);
+                key = (w << 15) | (uint32_t)k;
+            }
+            keys[k] = key;
+        }
+        __syncthreads();
+        for (int k = 2; k <= NPi; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < (NPi >> 1); i += blockDim.x) {
+                    const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+                    const int hi = lo + j;
+                    const bool up = (lo & k) == 0;
+                    const uint32_t x = keys[lo], y = keys[hi];
+                    if ((x > y) == up) { keys[lo] = y; keys[hi] = x; }
+                }
+                __syncthreads();
+            }
+        }
+        for (int r = threadIdx.x; r < n; r += blockDim.x) {
+            const int idx = (int)(keys[r] & 0x7fffu);
+            const int4 q = P.req[off + idx];
+            rq[off + r] = make_uint4((uint32_t)q.y, (uint32_t)q.w, (uint32_t)q.z, (uint32_t)idx);
+            arank[off + idx] = r;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace kv

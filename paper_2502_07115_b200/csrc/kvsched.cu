@@ -1,0 +1,525 @@
+// kvsched.cu -- C ABI of libkvsched.so (see include/kvsched.h for the contract).
+//
+// Host side: argument validation, size bounds, scratch management, kernel selection and
+// launch on the context's stream.  All simulation work runs in the kernels of
+// kernel_small.cuh / kernel_ring.cuh; there is no CPU path.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/kvsched.h"
+#include "kernel_ring.cuh"
+#include "kernel_small.cuh"
+
+using namespace kv;
+
+namespace {
+
+constexpr int kBlock = 128;                   // 4 warps, one instance per warp
+constexpr int kSmallMaxMem = 64;              // register profile covers tau = 1..64
+constexpr int kSmallMaxRequests = 16384;      // 14-bit idx in the packed word
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct sched_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    size_t max_smem_optin = 0;
+    char err[512] = {0};
+    const char *last_kernel = "";
+    DevBuf counter, bounds, rq, arank, pstart, total;
+    DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
+    // accounting
+    long long launches = 0, sim_launches = 0;
+    double sim_ms = 0.0;
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<cudaEvent_t> free_events;
+};
+
+static char g_init_err[512];
+
+static int fail(sched_ctx *c, int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c ? c->err : g_init_err, 512, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail((ctx), SCHED_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int grow(sched_ctx *c, DevBuf &b, size_t bytes)
+{
+    if (bytes <= b.bytes && b.p) return SCHED_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, SCHED_E_NOMEM, "cudaMalloc(%zu) failed", want);
+    }
+    b.bytes = want;
+    return SCHED_OK;
+}
+
+cudaEvent_t take_event(sched_ctx *c)
+{
+    if (!c->free_events.empty()) {
+        cudaEvent_t e = c->free_events.back();
+        c->free_events.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// ---- bounds: max requests per instance, max M, max(o, o~) -------------------------------
+__global__ void k_bounds(long long n_inst, const long long *off, const int4 *req, const int *mem, int *out)
+{
+    int mn = 0, mm = 0, ml = 0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_inst;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long lo = off[k], hi = off[k + 1];
+        mn = max(mn, (int)min(hi - lo, (long long)KV_INF));
+        mm = max(mm, mem[k]);
+        for (long long i = lo; i < hi; ++i) ml = max(ml, max(req[i].z, req[i].w));
+    }
+    mn = __reduce_max_sync(KV_FULL, mn);
+    mm = __reduce_max_sync(KV_FULL, mm);
+    ml = __reduce_max_sync(KV_FULL, ml);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out[0], mn);
+        atomicMax(&out[1], mm);
+        atomicMax(&out[2], ml);
+    }
+}
+
+// ---- TEL from a completion array: one warp per instance ---------------------------
+__global__ void __launch_bounds__(128) k_latency(long long n_inst, const long long *off, const int4 *req,
+                                                 const int *comp, long long *tel, unsigned long long *total)
+{
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_inst; k += warps) {
+        const long long lo = off[k], hi = off[k + 1];
+        long long s = 0;
+        bool neg = false;
+        for (long long i = lo + lane; i < hi; i += 32) {
+            const int c = comp[i];
+            neg |= c < 0;
+            s += (long long)c - req[i].x;
+        }
+        neg = __any_sync(KV_FULL, neg);
+        s = warp_sum_i64(s);
+        if (lane == 0) {
+            if (tel) tel[k] = neg ? -1 : s;
+            if (total && !neg) atomicAdd(total, (unsigned long long)s);
+        }
+    }
+}
+
+__global__ void k_philox(long long n, const uint4 *ctr, const uint2 *key, uint4 *out)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = philox4x32_10(ctr[i], key[i]);
+}
+
+template <typename K>
+int occupancy_grid(sched_ctx *c, K kernel, int smem, long long work_warps, int *grid)
+{
+    int per_sm = 0;
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
+    if (per_sm < 1) return fail(c, SCHED_E_ARG, "kernel does not fit one block per SM (smem %d B)", smem);
+    long long blocks = (work_warps + (kBlock / 32) - 1) / (kBlock / 32);
+    long long cap = (long long)per_sm * c->num_sms;
+    *grid = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+    return SCHED_OK;
+}
+
+template <typename K>
+int launch_sim(sched_ctx *c, K kernel, const KParams &P, int smem, const char *name)
+{
+    CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int grid = 1;
+    int rc = occupancy_grid(c, kernel, smem, P.n_inst, &grid);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    }
+    kernel<<<grid, kBlock, smem, c->stream>>>(P);
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->timing) {
+        CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+        c->pending.emplace_back(e0, e1);
+    }
+    c->launches++;
+    c->sim_launches++;
+    c->last_kernel = name;
+    return SCHED_OK;
+}
+
+int check_common(sched_ctx *c, const sched_instances *inst)
+{
+    if (!c) return SCHED_E_STATE;
+    if (!inst) return fail(c, SCHED_E_ARG, "inst is NULL");
+    if (inst->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
+    if (inst->reserved != 0) return fail(c, SCHED_E_ARG, "sched_instances.reserved must be 0");
+    if (inst->n_instances > 0) {
+        if (!inst->req_offset || !inst->mem_limit || !inst->req)
+            return fail(c, SCHED_E_ARG, "req_offset, req and mem_limit must be non-NULL");
+        if (((uintptr_t)inst->req) & 15u) return fail(c, SCHED_E_ARG, "req must be 16-byte aligned");
+    }
+    if (inst->max_requests < 0 || inst->max_mem < 0 || inst->max_len < 0)
+        return fail(c, SCHED_E_ARG, "size hints must be >= 0");
+    return SCHED_OK;
+}
+
+int check_policy(sched_ctx *c, const sched_policy *pol)
+{
+    if (!pol) return fail(c, SCHED_E_ARG, "pol is NULL");
+    if (pol->policy < SCHED_MCSF || pol->policy > SCHED_ALPHA_BETA)
+        return fail(c, SCHED_E_ARG, "unknown policy %d", pol->policy);
+    if (pol->reserved != 0) return fail(c, SCHED_E_ARG, "sched_policy.reserved must be 0");
+    if (pol->policy >= SCHED_ALPHA) {
+        if (pol->alpha_den <= 0 || pol->alpha_num < 0 || pol->alpha_num >= pol->alpha_den)
+            return fail(c, SCHED_E_ARG, "alpha = %d/%d must lie in [0, 1)", pol->alpha_num, pol->alpha_den);
+        if (pol->beta_thresh > (1ull << 32)) return fail(c, SCHED_E_ARG, "beta_thresh must be <= 2^32");
+    }
+    return SCHED_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+int sched_abi_version(void) { return KVSCHED_ABI_VERSION; }
+
+int sched_init(sched_ctx **out, int device, void *cuda_stream)
+{
+    if (!out) return fail(nullptr, SCHED_E_ARG, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, SCHED_E_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= ndev) return fail(nullptr, SCHED_E_ARG, "device %d out of range", device);
+    sched_ctx *c = new sched_ctx();
+    c->device = device;
+    c->stream = (cudaStream_t)cuda_stream;
+    DeviceGuard g(device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        delete c;
+        return fail(nullptr, SCHED_E_CUDA, "cudaGetDeviceProperties failed");
+    }
+    if (prop.major < 10) {
+        delete c;
+        return fail(nullptr, SCHED_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                    device, prop.major, prop.minor);
+    }
+    c->num_sms = prop.multiProcessorCount;
+    c->max_smem_optin = prop.sharedMemPerBlockOptin;
+    if (grow(c, c->counter, 64) || grow(c, c->bounds, 64) || grow(c, c->total, 64)) {
+        delete c;
+        return fail(nullptr, SCHED_E_NOMEM, "scratch allocation failed");
+    }
+    *out = c;
+    return SCHED_OK;
+}
+
+int sched_set_stream(sched_ctx *c, void *cuda_stream)
+{
+    if (!c) return SCHED_E_STATE;
+    c->stream = (cudaStream_t)cuda_stream;
+    return SCHED_OK;
+}
+
+int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
+                        const sched_outputs *out)
+{
+    int rc = check_common(c, inst);
+    if (rc) return rc;
+    if ((rc = check_policy(c, pol))) return rc;
+    if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
+    if (inst->n_instances == 0) return SCHED_OK;
+    DeviceGuard g(c->device);
+
+    int max_req = inst->max_requests, max_mem = inst->max_mem, max_len = inst->max_len;
+    if (max_req == 0 || max_mem == 0 || max_len == 0) {
+        CUDA_TRY(c, cudaMemsetAsync(c->bounds.p, 0, 16, c->stream));
+        long long blocks = (inst->n_instances + 255) / 256;
+        if (blocks > 4 * (long long)c->num_sms) blocks = 4 * (long long)c->num_sms;
+        k_bounds<<<(int)blocks, 256, 0, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
+                                                     reinterpret_cast<const int4 *>(inst->req),
+                                                     inst->mem_limit, (int *)c->bounds.p);
+        CUDA_TRY(c, cudaGetLastError());
+        c->launches++;
+        int hb[4];
+        CUDA_TRY(c, cudaMemcpyAsync(hb, c->bounds.p, 16, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        if (max_req == 0) max_req = hb[0];
+        if (max_mem == 0) max_mem = hb[1];
+        if (max_len == 0) max_len = hb[2];
+    }
+    if (max_req > SCHED_MAX_REQUESTS_PER_INSTANCE)
+        return fail(c, SCHED_E_ARG, "an instance has %d requests; limit %d", max_req, SCHED_MAX_REQUESTS_PER_INSTANCE);
+    if (max_len > SCHED_MAX_LEN) return fail(c, SCHED_E_ARG, "request length %d exceeds limit %d", max_len, SCHED_MAX_LEN);
+    if (max_req < 1) max_req = 1;
+    if (max_len < 1) max_len = 1;
+
+    KParams P;
+    memset(&P, 0, sizeof(P));
+    P.n_inst = inst->n_instances;
+    P.offset = reinterpret_cast<const long long *>(inst->req_offset);
+    P.req = reinterpret_cast<const int4 *>(inst->req);
+    P.mem = inst->mem_limit;
+    P.id0 = (unsigned long long)inst->instance_id0;
+    P.policy = pol->policy;
+    P.alpha_num = pol->alpha_num;
+    P.alpha_den = pol->alpha_den > 0 ? pol->alpha_den : 1;
+    P.beta_thresh = pol->beta_thresh;
+    P.seed = pol->seed;
+    P.round_cap = pol->round_cap;
+    P.max_requests = max_req;
+    P.max_mem = max_mem;
+    P.max_len = max_len;
+    P.completion = out->completion;
+    P.start = out->start;
+    P.tel = reinterpret_cast<long long *>(out->tel);
+    P.rounds = reinterpret_cast<long long *>(out->rounds);
+    P.drounds = reinterpret_cast<long long *>(out->decision_rounds);
+    P.evictions = reinterpret_cast<long long *>(out->evictions);
+    P.makespan = out->makespan;
+    P.peak = out->peak_mem;
+    P.status = out->status;
+    P.counter = reinterpret_cast<unsigned long long *>(c->counter.p);
+    CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+
+    const bool mc = pol->policy == SCHED_MCSF || pol->policy == SCHED_MC_BENCH;
+    if (mc && max_mem <= kSmallMaxMem && max_req <= kSmallMaxRequests) {
+        P.NP = next_pow2(max_req < 32 ? 32 : max_req);
+        P.warp_bytes = small_warp_bytes(P.NP);
+        const int smem = P.warp_bytes * (kBlock / 32);
+        if ((size_t)smem > c->max_smem_optin)
+            return fail(c, SCHED_E_ARG, "small kernel needs %d B shared memory per block", smem);
+        return pol->policy == SCHED_MCSF ? launch_sim(c, k_mc_small<POL_MCSF>, P, smem, "k_mc_small<MCSF>")
+                                         : launch_sim(c, k_mc_small<POL_MCBENCH>, P, smem, "k_mc_small<MCBENCH>");
+    }
+
+    // ring kernel: profile ring L > max_len (and > M - 1 for the projection window)
+    P.NP = next_pow2(max_req < 32 ? 32 : max_req);
+    P.L = next_pow2(max_len + 1);
+    P.warp_bytes = ring_warp_bytes(P.L, P.NP, pol->policy);
+    const int smem = P.warp_bytes * (kBlock / 32);
+    if ((size_t)smem > c->max_smem_optin)
+        return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per block (L=%d, NP=%d)", smem, P.L, P.NP);
+    const size_t slots = (size_t)inst->n_instances * (size_t)max_req;
+    if (pol->policy == SCHED_MCSF) {
+        if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
+        // offsets are relative to the batch: scratch slot = request row (n_req <= slots)
+        P.rq = reinterpret_cast<const uint4 *>(c->rq.p);
+        P.arank = reinterpret_cast<const int *>(c->arank.p);
+        const int ssmem = next_pow2(max_req) * 4;
+        CUDA_TRY(c, cudaFuncSetAttribute(k_rank_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+        long long blocks = inst->n_instances < 4LL * c->num_sms ? inst->n_instances : 4LL * c->num_sms;
+        k_rank_sort<<<(int)blocks, 1024, ssmem, c->stream>>>(P, reinterpret_cast<uint4 *>(c->rq.p),
+                                                             reinterpret_cast<int *>(c->arank.p));
+        CUDA_TRY(c, cudaGetLastError());
+        c->launches++;
+        return launch_sim(c, k_ring<POL_MCSF>, P, smem, "k_ring<MCSF>");
+    }
+    if (pol->policy == SCHED_MC_BENCH) return launch_sim(c, k_ring<POL_MCBENCH>, P, smem, "k_ring<MCBENCH>");
+    if ((rc = grow(c, c->pstart, slots * 4))) return rc;
+    P.pstart = reinterpret_cast<int *>(c->pstart.p);
+    if (pol->policy == SCHED_ALPHA) return launch_sim(c, k_ring<POL_ALPHA>, P, smem, "k_ring<ALPHA>");
+    return launch_sim(c, k_ring<POL_ALPHA_BETA>, P, smem, "k_ring<ALPHA_BETA>");
+}
+
+int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
+                             const sched_outputs *out)
+{
+    int rc = check_common(c, inst);
+    if (rc) return rc;
+    if ((rc = check_policy(c, pol))) return rc;
+    if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
+    const long long ni = inst->n_instances;
+    if (ni == 0) return SCHED_OK;
+    DeviceGuard g(c->device);
+    const long long n_req = inst->req_offset[ni];
+    if (n_req < 0) return fail(c, SCHED_E_ARG, "req_offset[n] < 0");
+    const size_t b_off = (size_t)(ni + 1) * 8, b_req = (size_t)n_req * 16, b_mem = (size_t)ni * 4;
+    if ((rc = grow(c, c->h_off, b_off)) || (rc = grow(c, c->h_req, b_req)) || (rc = grow(c, c->h_mem, b_mem)))
+        return rc;
+    // device outputs: completion, start [n_req] int32; 4 x int64 + 3 x int32 per instance
+    const size_t o_comp = 0, o_start = o_comp + (size_t)n_req * 4, o_i64 = (o_start + (size_t)n_req * 4 + 15) & ~(size_t)15;
+    const size_t o_i32 = o_i64 + (size_t)ni * 8 * 4;
+    const size_t total = o_i32 + (size_t)ni * 4 * 3;
+    if ((rc = grow(c, c->h_out, total))) return rc;
+    char *ob = (char *)c->h_out.p;
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_off.p, inst->req_offset, b_off, cudaMemcpyHostToDevice, c->stream));
+    if (b_req) CUDA_TRY(c, cudaMemcpyAsync(c->h_req.p, inst->req, b_req, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_mem.p, inst->mem_limit, b_mem, cudaMemcpyHostToDevice, c->stream));
+    sched_instances di = *inst;
+    di.req_offset = (const int64_t *)c->h_off.p;
+    di.req = (const int32_t *)c->h_req.p;
+    di.mem_limit = (const int32_t *)c->h_mem.p;
+    sched_outputs dout;
+    dout.completion = out->completion ? (int32_t *)(ob + o_comp) : nullptr;
+    dout.start = out->start ? (int32_t *)(ob + o_start) : nullptr;
+    dout.tel = out->tel ? (int64_t *)(ob + o_i64) : nullptr;
+    dout.rounds = out->rounds ? (int64_t *)(ob + o_i64 + ni * 8) : nullptr;
+    dout.decision_rounds = out->decision_rounds ? (int64_t *)(ob + o_i64 + ni * 16) : nullptr;
+    dout.evictions = out->evictions ? (int64_t *)(ob + o_i64 + ni * 24) : nullptr;
+    dout.makespan = out->makespan ? (int32_t *)(ob + o_i32) : nullptr;
+    dout.peak_mem = out->peak_mem ? (int32_t *)(ob + o_i32 + ni * 4) : nullptr;
+    dout.status = out->status ? (int32_t *)(ob + o_i32 + ni * 8) : nullptr;
+    if ((rc = sched_run_instances(c, &di, pol, &dout))) return rc;
+    struct { void *h; const void *d; size_t b; } cp[] = {
+        {out->completion, dout.completion, (size_t)n_req * 4}, {out->start, dout.start, (size_t)n_req * 4},
+        {out->tel, dout.tel, (size_t)ni * 8}, {out->rounds, dout.rounds, (size_t)ni * 8},
+        {out->decision_rounds, dout.decision_rounds, (size_t)ni * 8}, {out->evictions, dout.evictions, (size_t)ni * 8},
+        {out->makespan, dout.makespan, (size_t)ni * 4}, {out->peak_mem, dout.peak_mem, (size_t)ni * 4},
+        {out->status, dout.status, (size_t)ni * 4}};
+    for (auto &x : cp)
+        if (x.h && x.b) CUDA_TRY(c, cudaMemcpyAsync(x.h, x.d, x.b, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return SCHED_OK;
+}
+
+int sched_latency(sched_ctx *c, const sched_instances *inst, const int32_t *completion, int64_t *tel,
+                  int64_t *tel_total)
+{
+    if (!c) return SCHED_E_STATE;
+    if (!inst) return fail(c, SCHED_E_ARG, "inst is NULL");
+    if (inst->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
+    DeviceGuard g(c->device);
+    if (tel_total) CUDA_TRY(c, cudaMemsetAsync(tel_total, 0, 8, c->stream));
+    if (inst->n_instances == 0) return SCHED_OK;
+    if (!inst->req_offset || !inst->req || !completion)
+        return fail(c, SCHED_E_ARG, "req_offset, req and completion must be non-NULL");
+    long long blocks = (inst->n_instances + 3) / 4;
+    if (blocks > 16LL * c->num_sms) blocks = 16LL * c->num_sms;
+    k_latency<<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances,
+                                                  reinterpret_cast<const long long *>(inst->req_offset),
+                                                  reinterpret_cast<const int4 *>(inst->req), completion,
+                                                  reinterpret_cast<long long *>(tel),
+                                                  reinterpret_cast<unsigned long long *>(tel_total));
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
+int sched_philox4x32_10(sched_ctx *c, int64_t n, const uint32_t *ctr, const uint32_t *key, uint32_t *out)
+{
+    if (!c) return SCHED_E_STATE;
+    if (n < 0 || (n > 0 && (!ctr || !key || !out))) return fail(c, SCHED_E_ARG, "bad arguments");
+    if (n == 0) return SCHED_OK;
+    DeviceGuard g(c->device);
+    k_philox<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, c->stream>>>(
+        n, reinterpret_cast<const uint4 *>(ctr), reinterpret_cast<const uint2 *>(key), reinterpret_cast<uint4 *>(out));
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
+int sched_set_timing(sched_ctx *c, int enable)
+{
+    if (!c) return SCHED_E_STATE;
+    c->timing = enable != 0;
+    return SCHED_OK;
+}
+
+int sched_get_stats(sched_ctx *c, int64_t *launches, double *sim_kernel_ms, int64_t *sim_kernel_launches)
+{
+    if (!c) return SCHED_E_STATE;
+    DeviceGuard g(c->device);
+    for (auto &p : c->pending) {
+        CUDA_TRY(c, cudaEventSynchronize(p.second));
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, p.first, p.second));
+        c->sim_ms += ms;
+        c->free_events.push_back(p.first);
+        c->free_events.push_back(p.second);
+    }
+    c->pending.clear();
+    if (launches) *launches = c->launches;
+    if (sim_kernel_ms) *sim_kernel_ms = c->sim_ms;
+    if (sim_kernel_launches) *sim_kernel_launches = c->sim_launches;
+    return SCHED_OK;
+}
+
+int sched_reset_stats(sched_ctx *c)
+{
+    if (!c) return SCHED_E_STATE;
+    double ms;
+    int rc = sched_get_stats(c, nullptr, &ms, nullptr);
+    c->launches = 0;
+    c->sim_launches = 0;
+    c->sim_ms = 0.0;
+    return rc;
+}
+
+const char *sched_last_kernel(const sched_ctx *c) { return c ? c->last_kernel : ""; }
+
+int sched_finalize(sched_ctx *c)
+{
+    if (!c) return SCHED_E_STATE;
+    {
+        DeviceGuard g(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->total, &c->h_off,
+                          &c->h_req, &c->h_mem, &c->h_out})
+            if (b->p) cudaFree(b->p);
+        for (auto &p : c->pending) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        for (auto e : c->free_events) cudaEventDestroy(e);
+    }
+    delete c;
+    return SCHED_OK;
+}
+
+const char *sched_last_error(const sched_ctx *c) { return c ? c->err : g_init_err; }
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// params.cuh -- launch parameters and the per-instance epilogue shared by the kernels.
+#pragma once
+#include <stdint.h>
+#include "common.cuh"
+
+namespace kv {
+
+enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3 };
+enum { ST_OK = 0, ST_INVALID = 1, ST_LIVELOCK = 2, ST_UNSUPPORTED = 3 };
+
+struct KParams {
+    // batch
+    long long n_inst;
+    const long long *offset;
+    const int4 *req;            // {a, s, o, o~}
+    const int *mem;
+    unsigned long long id0;
+    // policy
+    int policy, alpha_num, alpha_den;
+    unsigned long long beta_thresh, seed;
+    long long round_cap;
+    // capacity (validated hints)
+    int max_requests, max_mem, max_len;
+    int NP;                     // per-warp rank capacity (pow2 >= max_requests, >= 32)
+    int L;                      // ring kernel: profile ring length (pow2 > max_len)
+    int warp_bytes;             // dynamic shared memory per warp
+    // outputs (any may be null)
+    int *completion, *start;
+    long long *tel, *rounds, *drounds, *evictions;
+    int *makespan, *peak, *status;
+    // scratch
+    unsigned long long *counter; // persistent-grid work counter (zeroed before launch)
+    int *pstart;                // alpha policies: start round of each request (scratch)
+    const uint4 *rq;            // MC-SF ring path: per-rank entries {s, o~, o, idx}
+    const int *arank;           // MC-SF ring path: rank of request idx
+};
+
+// Lane 0 writes the per-instance outputs.
+__device__ __forceinline__ void write_result(const KParams &P, long long inst, const InstResult &r)
+{
+    if (lane_id() != 0) return;
+    const bool ok = r.status == ST_OK;
+    if (P.tel) P.tel[inst] = ok ? r.tel : -1;
+    if (P.rounds) P.rounds[inst] = ok ? r.rounds : -1;
+    if (P.drounds) P.drounds[inst] = r.decision_rounds;
+    if (P.evictions) P.evictions[inst] = r.evictions;
+    if (P.makespan) P.makespan[inst] = ok ? r.makespan : -1;
+    if (P.peak) P.peak[inst] = r.peak;
+    if (P.status) P.status[inst] = r.status;
+}
+
+// Every request of an instance rejected before simulation: completion = start = -1.
+__device__ __forceinline__ void fill_unscheduled(const KParams &P, long long off, int n)
+{
+    for (int k = lane_id(); k < n; k += 32) {
+        if (P.completion) P.completion[off + k] = -1;
+        if (P.start) P.start[off + k] = -1;
+    }
+}
+
+__device__ __forceinline__ long long default_cap(long long amax, long long sum_o)
+{
+    long long cap = 16 * (amax + sum_o) + 64;          // DESIGN Q23
+    return cap > (1ll << 30) ? (1ll << 30) : cap;
+}
+
+}  // namespace kv

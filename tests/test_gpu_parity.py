@@ -1,0 +1,294 @@
+"""GPU parity: libkvsched.so (CUDA, through the C ABI) vs the CPU oracle, bit-exact.
+
+Every field the ABI returns -- per-request completion and start rounds, per-instance TEL,
+rounds, decision rounds, evictions, makespan, peak memory and status -- must equal the
+oracle's on the same seeded inputs.  All integer: the bar is byte equality.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+KIND = {0: "mcsf", 1: "mcbench", 2: "alpha", 3: "alpha_beta"}
+
+
+@pytest.fixture(scope="module")
+def K():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    import paper_2502_07115_b200 as K
+    from paper_2502_07115_b200 import build
+    build.build()
+    return K
+
+
+@pytest.fixture(scope="module")
+def ctx(K):
+    c = K.Context(0)
+    yield c
+    c.close()
+
+
+def oracle_run(O, b, pol, alpha=(0, 1), beta_thresh=0, seed=0, round_cap=0, gid0=0):
+    return O.simulate_batch(b.offset, b.req, b.mem, pol, alpha=alpha, beta_thresh=beta_thresh,
+                            seed=seed, round_cap=round_cap, gid0=gid0)
+
+
+def gpu_run(K, ctx, b, pol, alpha=(0, 1), beta_thresh=0, seed=0, round_cap=0, id0=0, hints=None):
+    p = K.Policy(KIND[pol], alpha, beta_thresh, seed, round_cap)
+    return K.simulate(ctx, b, p, id0=id0, hints=hints if hints is not None else K.hints_of(b))
+
+
+def assert_parity(o, g, b, label=""):
+    fields = [("completion", "completion"), ("start", "start"), ("tel", "tel"), ("rounds", "rounds"),
+              ("decision_rounds", "decision_rounds"), ("evictions", "evictions"),
+              ("makespan", "makespan"), ("peak", "peak_mem"), ("status", "status")]
+    for ok, gk in fields:
+        x, y = np.asarray(o[ok]), np.asarray(g[gk])
+        if not np.array_equal(x.astype(np.int64), y.astype(np.int64)):
+            bad = np.nonzero(x != y)[0]
+            i = int(bad[0])
+            if ok in ("completion", "start"):
+                k = int(np.searchsorted(b.offset, i, side="right") - 1)
+            else:
+                k = i
+            raise AssertionError(f"{label}: {ok} differs at {len(bad)} positions; first {i} "
+                                 f"(instance {k}): oracle {x[i]} gpu {y[i]}; "
+                                 f"oracle status {o['status'][k]} gpu status {g['status'][k]}")
+
+
+def check(K, ctx, O, b, pol, label, **kw):
+    hints = kw.pop("hints", None)
+    o = oracle_run(O, b, pol, **{k: v for k, v in kw.items() if k != "id0"},
+                   gid0=kw.get("id0", 0))
+    g = gpu_run(K, ctx, b, pol, hints=hints, **kw)
+    assert_parity(o, g, b, label)
+    return o, g
+
+
+# ---------------------------------------------------------------------------------------
+def test_library_loaded_is_in_tree(K):
+    import paper_2502_07115_b200.kvsched as kv
+    lib = K.load()
+    assert Path(lib._name).resolve() == kv.LIB_PATH.resolve()
+
+
+@pytest.mark.parametrize("case", json.loads((GOLDEN / "worked_examples.json").read_text())["cases"],
+                         ids=lambda c: c["name"])
+def test_worked_examples_on_gpu(K, ctx, oracle_mod, case):
+    pol = {"mcsf": 0, "mcbench": 1, "alpha": 2, "alpha_beta": 3}[case["policy"]]
+    b = W.from_instances([(case["req"], case["M"])])
+    alpha = tuple(case.get("alpha", (0, 1)))
+    o, g = check(K, ctx, oracle_mod, b, pol, case["name"], alpha=alpha)
+    for k, v in case["expect"].items():
+        gk = "peak_mem" if k == "peak" else k
+        got = g[gk] if k in ("completion", "start") else g[gk][0]
+        assert (list(got) == v) if isinstance(v, list) else (got == v), (k, got, v)
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+@pytest.mark.parametrize("variant", ["a", "b"])
+def test_c1_tiny(K, ctx, oracle_mod, pol, variant):
+    b = W.c1(4000, 11, variant)
+    check(K, ctx, oracle_mod, b, pol, f"C1{variant}")
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_c2_am1(K, ctx, oracle_mod, pol):
+    b = W.am1(48, 12)
+    check(K, ctx, oracle_mod, b, pol, "C2")
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_c5_am2(K, ctx, oracle_mod, pol):
+    b = W.am2(6000, 13)
+    check(K, ctx, oracle_mod, b, pol, "C5")
+
+
+def test_am1_paper_draw(K, ctx, oracle_mod):
+    b = W.am1_paper(400, 14)
+    check(K, ctx, oracle_mod, b, 0, "AM1-paper")
+
+
+@pytest.mark.parametrize("pol", [0, 1, 2, 3])
+@pytest.mark.parametrize("mhi", [64, 300])
+def test_fuzz_ragged(K, ctx, oracle_mod, pol, mhi):
+    """Ragged batches (empty instances included), M up to 64 (fused kernel for MC) and up to
+    300 (ring kernel)."""
+    b = W.random_small(3000, 15 + mhi, n_max=70, M_lo=4, M_hi=mhi, a_max=60)
+    assert (b.sizes() == 0).any()
+    kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=77) if pol >= 2 else {}
+    check(K, ctx, oracle_mod, b, pol, f"fuzz M<={mhi}", **kw)
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_ring_kernel_on_small_budgets(K, ctx, oracle_mod, pol):
+    """Force the shared-memory ring kernel (hint max_mem > 64) on small-M instances: both
+    kernels must reproduce the oracle."""
+    b = W.random_small(3000, 16, n_max=70, M_lo=4, M_hi=64, a_max=60)
+    check(K, ctx, oracle_mod, b, pol, "ring on small M", hints=(70, 65, 64))
+    c = W.am2(2000, 17)
+    check(K, ctx, oracle_mod, c, pol, "ring on C5", hints=(c.max_requests(), 65, 64))
+
+
+def test_prediction_overestimate_small(K, ctx, oracle_mod):
+    """MC-SF with o~ >= o: early completions remove the unused projected tail."""
+    b = W.random_small(3000, 18, n_max=50, M_lo=8, M_hi=64, a_max=40, pred_slack=8)
+    assert (b.req[:, 3] > b.req[:, 2]).any()
+    check(K, ctx, oracle_mod, b, 0, "o~ > o")
+
+
+@pytest.mark.parametrize("name,pol,alpha,beta", W.C4_POLICIES, ids=[p[0] for p in W.C4_POLICIES])
+def test_c4_policies(K, ctx, oracle_mod, name, pol, alpha, beta):
+    b = W.c4(48, 19)
+    polid = {"mcsf": 0, "mcbench": 1, "alpha": 2, "alpha_beta": 3}[pol]
+    kw = dict(alpha=alpha or (0, 1), beta_thresh=W.beta_threshold(beta or 0.0), seed=2025)
+    check(K, ctx, oracle_mod, b, polid, name, **kw)
+
+
+@pytest.mark.parametrize("pol", [2, 3])
+def test_alpha_with_evictions(K, ctx, oracle_mod, pol):
+    """Tight budgets force overflows, evictions and (for alpha-greedy) livelocks."""
+    b = W.random_small(3000, 20, n_max=40, M_lo=10, M_hi=80, a_max=20)
+    for alpha in ((1, 10), (0, 1), (3, 10)):
+        o, g = check(K, ctx, oracle_mod, b, pol, f"alpha={alpha}", alpha=alpha,
+                     beta_thresh=W.beta_threshold(0.25), seed=5)
+    assert o["evictions"].sum() > 0
+    assert (o["status"] == 2).any() or pol == 3
+
+
+@pytest.mark.parametrize("lam", [0.4, 2.0])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_c3_trace(K, ctx, oracle_mod, lam, pol):
+    b = W.c3(2, 21, lam)
+    check(K, ctx, oracle_mod, b, pol, f"C3 lam={lam}")
+
+
+@pytest.mark.parametrize("pol", [0, 1, 2, 3])
+def test_round_cap_livelock(K, ctx, oracle_mod, pol):
+    """An explicit round cap stops runs mid-flight: both sides report LIVELOCK with the same
+    partial counters and completions."""
+    b = W.random_small(2000, 22, n_max=40, M_lo=6, M_hi=120, a_max=30)
+    for cap in (5, 17, 40):
+        kw = dict(round_cap=cap)
+        if pol >= 2:
+            kw.update(alpha=(1, 10), beta_thresh=W.beta_threshold(0.4), seed=3)
+        o, _ = check(K, ctx, oracle_mod, b, pol, f"cap={cap}", **kw)
+        assert (o["status"] == 2).any()
+
+
+@pytest.mark.parametrize("pol", [0, 1, 2, 3])
+def test_invalid_instances(K, ctx, oracle_mod, pol):
+    insts = [([[0, 5, 6, 6]], 10), ([[3, 1, 1, 1], [2, 1, 1, 1]], 10), ([[0, 0, 1, 1]], 10),
+             ([[0, 1, 3, 2]], 10), ([], 7), ([[0, 1, 1, 1]] * 3, 6), ([[0, 2, 3, 3], [1, 60, 3, 3]], 62),
+             ([[0, 1, 2, 2], [0, 1, 2, 2], [0, 1, 5, 5]], 6)]
+    b = W.from_instances(insts)
+    check(K, ctx, oracle_mod, b, pol, "invalid", alpha=(1, 4), beta_thresh=2**31, seed=9)
+
+
+def test_shard_invariance(K, ctx, oracle_mod):
+    """Outputs do not depend on how the batch is split (instance_id0 keys the RNG)."""
+    b = W.random_small(1500, 23, n_max=40, M_lo=10, M_hi=80, a_max=20)
+    kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=11)
+    whole = gpu_run(K, ctx, b, 3, **kw)
+    cut = 611
+    lo, hi = b.subset(range(cut)), b.subset(range(cut, b.n_inst))
+    g0 = gpu_run(K, ctx, lo, 3, id0=0, **kw)
+    g1 = gpu_run(K, ctx, hi, 3, id0=cut, **kw)
+    for k in ("tel", "evictions", "status"):
+        assert np.array_equal(whole[k], np.concatenate([g0[k], g1[k]]))
+    assert np.array_equal(whole["completion"], np.concatenate([g0["completion"], g1["completion"]]))
+    o1 = oracle_run(oracle_mod, hi, 3, gid0=cut, **kw)
+    assert np.array_equal(o1["completion"], g1["completion"])
+
+
+def test_unmeasured_hints(K, ctx, oracle_mod):
+    """hints = 0 -> the library measures the bounds itself."""
+    b = W.random_small(500, 24, n_max=50, M_lo=4, M_hi=200)
+    o = oracle_run(oracle_mod, b, 0)
+    g = gpu_run(K, ctx, b, 0, hints=(0, 0, 0))
+    assert_parity(o, g, b, "measured hints")
+
+
+def test_hint_violation_is_unsupported(K, ctx):
+    b = W.random_small(200, 25, n_max=50, M_lo=20, M_hi=60)
+    g = gpu_run(K, ctx, b, 0, hints=(20, 64, 63))
+    big = b.sizes() > 20
+    assert (g["status"][big] == 3).all() and (g["status"][~big] != 3).all()
+
+
+def test_latency_kernel(K, ctx, oracle_mod):
+    import torch
+    b = W.am2(3000, 26)
+    o = oracle_run(oracle_mod, b, 0)
+    dev = torch.device("cuda", 0)
+    off, req, _ = K.to_device(b, dev)
+    comp = torch.from_numpy(o["completion"]).to(dev)
+    tel = torch.empty(b.n_inst, dtype=torch.int64, device=dev)
+    tot = torch.empty(1, dtype=torch.int64, device=dev)
+    ctx.latency(off, req, comp, tel, tot)
+    torch.cuda.synchronize()
+    assert np.array_equal(tel.cpu().numpy(), o["tel"])
+    assert int(tot.item()) == int(o["tel"].sum())
+    comp[5] = -1
+    ctx.latency(off, req, comp, tel, tot)
+    torch.cuda.synchronize()
+    k = int(np.searchsorted(b.offset, 5, side="right") - 1)
+    assert tel[k].item() == -1
+
+
+def test_philox_known_answers_device(K, ctx):
+    import torch
+    ctr = torch.tensor([[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]],
+                       dtype=torch.int64).to(torch.uint32).cuda()
+    key = torch.tensor([[0, 0], [0xFFFFFFFF] * 2, [0xA4093822, 0x299F31D0]], dtype=torch.int64).to(torch.uint32).cuda()
+    out = torch.zeros((3, 4), dtype=torch.uint32, device="cuda")
+    ctx.philox(ctr, key, out)
+    torch.cuda.synchronize()
+    got = out.cpu().to(torch.int64).numpy().tolist()
+    assert got[0] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert got[1] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert got[2] == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_host_path(K, ctx, oracle_mod):
+    """sched_run_instances_host (host buffers, copies inside the call) gives the same bytes."""
+    import paper_2502_07115_b200.kvsched as kv
+    b = W.am2(2000, 27)
+    o = oracle_run(oracle_mod, b, 0)
+    outs = {"completion": np.empty(b.n_req, np.int32), "start": np.empty(b.n_req, np.int32)}
+    for k in ("tel", "rounds", "decision_rounds", "evictions"):
+        outs[k] = np.empty(b.n_inst, np.int64)
+    for k in ("makespan", "peak_mem", "status"):
+        outs[k] = np.empty(b.n_inst, np.int32)
+    ctx.run_host(b.offset, b.req, b.mem, kv.Policy("mcsf"), outs, hints=K.hints_of(b))
+    assert_parity(o, outs, b, "host path")
+
+
+def test_full_size_c5_sampled(K, ctx, oracle_mod):
+    """The bench configuration at full size (10^6 AM2 instances, one launch as bench.py
+    times it); 300 sampled instances recomputed one by one by the oracle."""
+    import torch
+    b = W.am2(1_000_000, 5)
+    dev = torch.device("cuda", 0)
+    off, req, mem = K.to_device(b, dev)
+    out = K.alloc_outputs(b.n_inst, b.n_req, dev)
+    ctx.run(off, req, mem, K.Policy("mcsf"), out, hints=K.hints_of(b))
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    assert (g["status"][:b.n_inst] == 0).all()
+    ks = np.random.default_rng(0).choice(b.n_inst, 300, replace=False)
+    ks[:2] = [0, b.n_inst - 1]
+    for k in ks:
+        req_k, M = b.instance(int(k))
+        o = oracle_mod.simulate(req_k, M, 0)
+        lo, hi = int(b.offset[k]), int(b.offset[k + 1])
+        assert np.array_equal(o["completion"], g["completion"][lo:hi])
+        assert o["tel"] == g["tel"][k] and o["rounds"] == g["rounds"][k]
+        assert o["peak"] == g["peak_mem"][k] and o["decision_rounds"] == g["decision_rounds"][k]
