@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ab", action="store_true",
+                    help="also time SCHED_FLAG_PER_ROUND (one Eq. 5 evaluation per round)")
     return ap.parse_args()
 
 
@@ -254,6 +256,7 @@ def main():
     torch.cuda.synchronize(dev)
     rounds_rank = int(out["rounds"][:batch.n_inst].clamp(min=0).sum().item())
     ok_rank = int((out["status"][:batch.n_inst] == 0).sum().item())
+    drounds_rank = int(out["decision_rounds"][:batch.n_inst].sum().item())
 
     clocks = Clocks(local)
     ctx.reset_stats()
@@ -330,6 +333,22 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": e_ms / args.e2e_steps, "matches_device_run": bool(same)}
 
+    ab = None
+    if args.ab:
+        pr = K.Policy(pol.kind, pol.alpha, pol.beta_thresh, pol.seed, pol.round_cap, K.kvsched.FLAG_PER_ROUND)
+        ctx.run(off, req, mem, pr, out, id0=id0, hints=hints)
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            ctx.run(off, req, mem, pr, out, id0=id0, hints=hints)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        ab_ms = g0.elapsed_time(g1) / args.steps
+        ab = {"per_round_kernel": ctx.last_kernel(), "per_round_ms_per_step": ab_ms,
+              "per_round_value": rounds_rank * world / (ab_ms / 1000.0),
+              "speedup_of_default": ab_ms / (ms_max / args.steps)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(batch, args.policy, args.cpu_seconds, gid0=id0)
@@ -344,7 +363,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
                 "config": cfg, "instances_per_s": inst_all * args.steps / (ms_max / 1000.0),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
-                "gpu_launches": st["launches"]}
+                "gpu_launches": st["launches"], "decision_rounds_per_step": drounds_rank * world,
+                "ab": ab}
         print(json.dumps(line))
     ctx.close()
     if world > 1:

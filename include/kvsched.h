@@ -75,6 +75,11 @@ enum {
 #define SCHED_MAX_REQUESTS_PER_INSTANCE 32768
 #define SCHED_MAX_LEN 32767     /* max over requests of max(o, o~), also bounds M - 1 use */
 
+/* sched_policy.flags.  SCHED_FLAG_PER_ROUND makes the MC kernels evaluate Eq. 5 for one
+ * round per loop iteration instead of resolving a blocked queue head over up to 64
+ * rounds in one warp pass (same results; for A/B measurement).                          */
+#define SCHED_FLAG_PER_ROUND 1
+
 typedef struct sched_ctx sched_ctx;   /* opaque: device, stream, scratch, timers */
 
 /* A batch of independent instances in CSR form.                                        */
@@ -100,7 +105,7 @@ typedef struct {
     int32_t policy;             /* SCHED_MCSF .. SCHED_ALPHA_BETA                            */
     int32_t alpha_num;          /* alpha = alpha_num / alpha_den in [0, 1) (alpha policies);  */
     int32_t alpha_den;          /*   budget B = ((den - num) * M) / den (DESIGN Q15)         */
-    int32_t reserved;           /* must be 0                                                 */
+    int32_t flags;              /* SCHED_FLAG_* bits, 0 = defaults                           */
     uint64_t beta_thresh;       /* alpha-beta: evict iff u32 draw < beta_thresh, in [0, 2^32];
                                    round(beta * 2^32); 2^32 = always (beta = 1)              */
     uint64_t seed;              /* alpha-beta RNG key                                        */

@@ -75,7 +75,33 @@ __device__ __forceinline__ int prof_max(int P0, int P1, int d)
     return warp_max_i32(v);
 }
 
-template <int POL>
+// Bit D (0 <= D < 64) of the result is set iff a head candidate (s, w) would violate
+// Eq. 5 at round t+D while the profile only advances (no admission, arrival or early
+// completion in between).  Position u = t+D+tau of the profile rules out the offsets
+// D in [u-w, u-1] with Prof(u) + s + (u - D) > M, i.e. D <= Prof(u) + u - (M-s) - 1; the
+// union over the 64 positions held by the warp is two OR-reductions.  Prof is zero
+// beyond tau = 63 (o~ <= 63), so the head always fits by D = 64.
+__device__ __forceinline__ unsigned long long blocked_rounds(int P0, int P1, int s, int w, int M)
+{
+    const int lane = lane_id();
+    const int room = M - s;
+    unsigned long long m = 0ull;
+    {
+        const int u = lane + 1;
+        const int lo = max(0, u - w), hi = min(u - 1, P0 + u - room - 1);
+        if (hi >= lo) m |= (~0ull >> (63 - hi)) & (~0ull << lo);
+    }
+    {
+        const int u = lane + 33;
+        const int lo = max(0, u - w), hi = min(u - 1, P1 + u - room - 1);
+        if (hi >= lo) m |= (~0ull >> (63 - hi)) & (~0ull << lo);
+    }
+    const unsigned lo32 = __reduce_or_sync(KV_FULL, (unsigned)m);
+    const unsigned hi32 = __reduce_or_sync(KV_FULL, (unsigned)(m >> 32));
+    return ((unsigned long long)hi32 << 32) | lo32;
+}
+
+template <int POL, bool MULTI>
 __device__ void small_instance(const KParams &P, long long inst, const SmallSmem &S)
 {
     const int lane = lane_id();
@@ -153,7 +179,8 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     __syncwarp();
     WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
 
-    const long long cap = P.round_cap > 0 ? P.round_cap : default_cap(S.arr[n - 1], sumo);
+    const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(S.arr[n - 1], sumo);
+    const int cap = (int)min(cap64, 0x7ffffffell);
 
     // ---- round loop --------------------------------------------------------------------
     int t = S.arr[0];
@@ -162,7 +189,8 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     uint32_t hkey = 0u;
     bool hstale = false;
     int P0 = 0, P1 = 0;              // Prof(t+lane+1), Prof(t+lane+33)
-    long long sumc = 0, rounds = 0, drounds = 0;
+    long long sumc = 0;
+    int rounds = 0, drounds = 0;
     int maxc = -1, peak = 0, status = ST_OK;
     // early-completion records (slow mode): one lane per in-flight request with o~ > o
     int rc = KV_INF, rs = 0, rp = 0, rw = 0;
@@ -171,16 +199,16 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
         if (h == KV_INF) {
             if (!slow) {
                 if (a_next == KV_INF) {                       // drain: S only, no arrivals
-                    const long long E = min((long long)maxc, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, (int)min(E - t, 64ll)));
+                    const int E = min(maxc, cap + 1);
+                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
                     if (maxc > t) rounds += maxc - t;
-                    if ((long long)maxc >= cap + 1) status = ST_LIVELOCK;
+                    if (maxc >= cap + 1) status = ST_LIVELOCK;
                     break;
                 }
                 const int tn = a_next;
                 if (tn > t) {                                 // skip rounds t..tn-1
-                    const long long E = min((long long)tn, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, (int)min(E - t, 64ll)));
+                    const int E = min(tn, cap + 1);
+                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
                     rounds += max(0, min(tn, maxc) - t);
                     if (tn > cap) { status = ST_LIVELOCK; break; }
                     prof_shift(P0, P1, tn - t);
@@ -223,42 +251,69 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
                 if (lane + 33 <= e_) P1 -= s_ + t + lane + 33 - p_;
                 if (lane == l) rc = KV_INF;
             }
+            if (h == KV_INF) {                 // R empty, S non-empty: one plain round
+                if (maxc > t) ++rounds;
+                peak = max(peak, __shfl_sync(KV_FULL, P0, 0));
+                prof_shift1(P0, P1);
+                ++t;
+                continue;
+            }
         }
 
-        const bool had_R = h != KV_INF;
-        if (had_R) {
-            ++drounds;
-            if (hstale) { hkey = S.keys[h]; hstale = false; }
-            // Alg. 1 / Alg. 2: candidates in rank order, break at the first failure
-            for (;;) {
-                const int w = (POL == POL_MCSF) ? (int)(hkey >> 26) : (int)(hkey & 63u);
-                const int s = (int)((hkey >> 6) & 63u), o = (int)(hkey & 63u);
+        // decision round t with R non-empty (Alg. 1 / Alg. 2): candidates in rank order,
+        // break at the first failure.  The failing head keeps failing -- and nothing else
+        // is admitted -- until it fits, a request arrives or (o~ > o) a request completes
+        // early; the coverage test finds the first of those rounds in one pass.
+        if (hstale) { hkey = S.keys[h]; hstale = false; }
+        int jump = 1;
+        for (;;) {
+            const int w = (POL == POL_MCSF) ? (int)(hkey >> 26) : (int)(hkey & 63u);
+            const int s = (int)((hkey >> 6) & 63u), o = (int)(hkey & 63u);
+            if (MULTI) {
+                const unsigned long long cov = blocked_rounds(P0, P1, s, w, M);
+                if (cov & 1ull) {                                        // Eq. 5 violated now
+                    jump = (~cov == 0ull) ? 64 : __ffsll((long long)~cov) - 1;
+                    break;
+                }
+            } else {
                 const int tau0 = lane + 1, tau1 = lane + 33;
                 const bool v = (tau0 <= w && P0 + s + tau0 > M) || (tau1 <= w && P1 + s + tau1 > M);
                 if (__any_sync(KV_FULL, v)) break;                      // Eq. 5 violated
-                if (tau0 <= w) P0 += s + tau0;
-                if (tau1 <= w) P1 += s + tau1;
-                const int idx = (int)((hkey >> 12) & 0x3fffu);
-                const int c = t + o;                                     // c_i = p_i + o_i
-                if (lane == 0) {
-                    if (P.completion) P.completion[off + idx] = c;
-                    if (P.start) P.start[off + idx] = t;
-                }
-                sumc += c;
-                maxc = max(maxc, c);
-                if (POL == POL_MCSF && w > o) {                           // early completion
-                    const uint32_t fr = __ballot_sync(KV_FULL, rc == KV_INF);
-                    if (lane == __ffs(fr) - 1) { rc = c; rs = s; rp = t; rw = w; }
-                }
-                h = q_pop_head(Q, h);
-                if (h == KV_INF) break;
-                hkey = S.keys[h];
             }
+            if (lane + 1 <= w) P0 += s + lane + 1;                       // ramp s + tau (Eq. 3)
+            if (lane + 33 <= w) P1 += s + lane + 33;
+            const int idx = (int)((hkey >> 12) & 0x3fffu);
+            const int c = t + o;                                         // c_i = p_i + o_i
+            if (lane == 0) {
+                if (P.completion) P.completion[off + idx] = c;
+                if (P.start) P.start[off + idx] = t;
+            }
+            sumc += c;
+            maxc = max(maxc, c);
+            if (POL == POL_MCSF && w > o) {                               // early completion
+                const uint32_t fr = __ballot_sync(KV_FULL, rc == KV_INF);
+                if (lane == __ffs(fr) - 1) { rc = c; rs = s; rp = t; rw = w; }
+            }
+            h = q_pop_head(Q, h);
+            if (h == KV_INF) break;
+            hkey = S.keys[h];
         }
-        if (had_R || maxc > t) ++rounds;
-        peak = max(peak, __shfl_sync(KV_FULL, P0, 0));                   // Mem(t+1)
-        prof_shift1(P0, P1);
-        ++t;
+        if (MULTI && jump > 1) {
+            jump = min(jump, a_next - t);                 // a new request may become the head
+            jump = min(jump, cap + 1 - t);
+            if (slow) jump = min(jump, warp_min_i32(rc) - t);
+        }
+        // rounds t .. t+jump-1: decision rounds (R non-empty), batch memory Prof(t+1..t+jump)
+        drounds += jump;
+        rounds += jump;
+        if (jump == 1) {
+            peak = max(peak, __shfl_sync(KV_FULL, P0, 0));               // Mem(t+1)
+            prof_shift1(P0, P1);
+        } else {
+            peak = max(peak, prof_max(P0, P1, jump));
+            prof_shift(P0, P1, jump);
+        }
+        t += jump;
     }
 
     if (status != ST_OK) {
@@ -287,7 +342,7 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     write_result(P, inst, res);
 }
 
-template <int POL>
+template <int POL, bool MULTI>
 __global__ void __launch_bounds__(128) k_mc_small(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -307,7 +362,7 @@ __global__ void __launch_bounds__(128) k_mc_small(const KParams P)
     while (inst < P.n_inst) {
         long long nxt = 0;     // claim the next instance now; the latency hides behind this one
         if (lane == 0) nxt = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
-        small_instance<POL>(P, inst, S);
+        small_instance<POL, MULTI>(P, inst, S);
         inst = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();
     }

@@ -216,7 +216,7 @@ int check_policy(sched_ctx *c, const sched_policy *pol)
     if (!pol) return fail(c, SCHED_E_ARG, "pol is NULL");
     if (pol->policy < SCHED_MCSF || pol->policy > SCHED_ALPHA_BETA)
         return fail(c, SCHED_E_ARG, "unknown policy %d", pol->policy);
-    if (pol->reserved != 0) return fail(c, SCHED_E_ARG, "sched_policy.reserved must be 0");
+    if (pol->flags & ~SCHED_FLAG_PER_ROUND) return fail(c, SCHED_E_ARG, "unknown flags 0x%x", pol->flags);
     if (pol->policy >= SCHED_ALPHA) {
         if (pol->alpha_den <= 0 || pol->alpha_num < 0 || pol->alpha_num >= pol->alpha_den)
             return fail(c, SCHED_E_ARG, "alpha = %d/%d must lie in [0, 1)", pol->alpha_num, pol->alpha_den);
@@ -342,8 +342,12 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
         const int smem = P.warp_bytes * (kBlock / 32);
         if ((size_t)smem > c->max_smem_optin)
             return fail(c, SCHED_E_ARG, "small kernel needs %d B shared memory per block", smem);
-        return pol->policy == SCHED_MCSF ? launch_sim(c, k_mc_small<POL_MCSF>, P, smem, "k_mc_small<MCSF>")
-                                         : launch_sim(c, k_mc_small<POL_MCBENCH>, P, smem, "k_mc_small<MCBENCH>");
+        const bool per_round = pol->flags & SCHED_FLAG_PER_ROUND;
+        if (pol->policy == SCHED_MCSF)
+            return per_round ? launch_sim(c, k_mc_small<POL_MCSF, false>, P, smem, "k_mc_small<MCSF,per-round>")
+                             : launch_sim(c, k_mc_small<POL_MCSF, true>, P, smem, "k_mc_small<MCSF>");
+        return per_round ? launch_sim(c, k_mc_small<POL_MCBENCH, false>, P, smem, "k_mc_small<MCBENCH,per-round>")
+                         : launch_sim(c, k_mc_small<POL_MCBENCH, true>, P, smem, "k_mc_small<MCBENCH>");
     }
 
     // ring kernel: profile ring L > max_len (and > M - 1 for the projection window)

@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libkvsched.so"
 MCSF, MC_BENCH, ALPHA, ALPHA_BETA = 0, 1, 2, 3
 POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": ALPHA_BETA}
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
+FLAG_PER_ROUND = 1
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}
 
 # every symbol include/kvsched.h declares
@@ -37,7 +38,7 @@ class SchedInstances(ctypes.Structure):
 
 
 class SchedPolicy(ctypes.Structure):
-    _fields_ = [("policy", i32), ("alpha_num", i32), ("alpha_den", i32), ("reserved", i32),
+    _fields_ = [("policy", i32), ("alpha_num", i32), ("alpha_den", i32), ("flags", i32),
                 ("beta_thresh", u64), ("seed", u64), ("round_cap", i64)]
 
 
@@ -91,9 +92,10 @@ class Policy:
     beta_thresh: int = 0
     seed: int = 0
     round_cap: int = 0
+    flags: int = 0            # FLAG_PER_ROUND: one round per loop iteration (A/B runs)
 
     def as_c(self) -> SchedPolicy:
-        return SchedPolicy(POLICY_IDS[self.kind], int(self.alpha[0]), int(self.alpha[1]), 0,
+        return SchedPolicy(POLICY_IDS[self.kind], int(self.alpha[0]), int(self.alpha[1]), int(self.flags),
                            int(self.beta_thresh), int(self.seed) & (2**64 - 1), int(self.round_cap))
 
 

@@ -40,8 +40,9 @@ def oracle_run(O, b, pol, alpha=(0, 1), beta_thresh=0, seed=0, round_cap=0, gid0
                             seed=seed, round_cap=round_cap, gid0=gid0)
 
 
-def gpu_run(K, ctx, b, pol, alpha=(0, 1), beta_thresh=0, seed=0, round_cap=0, id0=0, hints=None):
-    p = K.Policy(KIND[pol], alpha, beta_thresh, seed, round_cap)
+def gpu_run(K, ctx, b, pol, alpha=(0, 1), beta_thresh=0, seed=0, round_cap=0, id0=0, hints=None,
+            flags=0):
+    p = K.Policy(KIND[pol], alpha, beta_thresh, seed, round_cap, flags)
     return K.simulate(ctx, b, p, id0=id0, hints=hints if hints is not None else K.hints_of(b))
 
 
@@ -65,7 +66,7 @@ def assert_parity(o, g, b, label=""):
 
 def check(K, ctx, O, b, pol, label, **kw):
     hints = kw.pop("hints", None)
-    o = oracle_run(O, b, pol, **{k: v for k, v in kw.items() if k != "id0"},
+    o = oracle_run(O, b, pol, **{k: v for k, v in kw.items() if k not in ("id0", "flags")},
                    gid0=kw.get("id0", 0))
     g = gpu_run(K, ctx, b, pol, hints=hints, **kw)
     assert_parity(o, g, b, label)
@@ -109,6 +110,23 @@ def test_c2_am1(K, ctx, oracle_mod, pol):
 def test_c5_am2(K, ctx, oracle_mod, pol):
     b = W.am2(6000, 13)
     check(K, ctx, oracle_mod, b, pol, "C5")
+
+
+@pytest.mark.parametrize("maker", ["c5", "c2", "fuzz", "slow", "c1b", "cap"])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_per_round_and_multi_round_modes(K, ctx, oracle_mod, maker, pol):
+    """SCHED_FLAG_PER_ROUND (one Eq. 5 evaluation per round) and the default (a blocked head
+    resolved over up to 64 rounds per warp pass) must both equal the oracle."""
+    b = {"c5": lambda: W.am2(3000, 31), "c2": lambda: W.am1(16, 32),
+         "fuzz": lambda: W.random_small(3000, 33, n_max=60, M_lo=4, M_hi=64, a_max=80),
+         "slow": lambda: W.random_small(3000, 34, n_max=50, M_lo=8, M_hi=64, a_max=40, pred_slack=9),
+         "c1b": lambda: W.c1(3000, 35, "b"),
+         "cap": lambda: W.random_small(2000, 36, n_max=40, M_lo=6, M_hi=64, a_max=30)}[maker]()
+    if maker == "slow" and pol == 1:
+        return
+    kw = dict(round_cap=23) if maker == "cap" else {}
+    for flags in (0, 1):
+        check(K, ctx, oracle_mod, b, pol, f"{maker} flags={flags}", flags=flags, **kw)
 
 
 def test_am1_paper_draw(K, ctx, oracle_mod):
