@@ -359,11 +359,11 @@ __global__ void __launch_bounds__(128) k_ring(const KParams P)
     S.infl = reinterpret_cast<uint32_t *>(base + P.L * 4 + (P.NP / 32) * 4 + 128);
 
     long long inst = 0;
-    if (lane == 0) inst = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
+    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
     inst = __shfl_sync(KV_FULL, inst, 0);
     while (inst < P.n_inst) {
         long long nxt = 0;
-        if (lane == 0) nxt = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
+        if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
         ring_instance<POL>(P, inst, S);
         inst = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();

@@ -5,44 +5,124 @@
 //   * projected memory profile Prof(t+tau), tau = 1..64, in registers: lane l holds
 //     tau = l+1 (P0) and tau = l+33 (P1).  Prof is the left-hand side of Eq. 5
 //     for the in-flight set S, so a candidate (s, w) is admissible at round t iff
-//         Prof(t+tau) + s + tau <= M  for every tau in [1, w]
-//     -- one vote over the warp.  With o~ >= o the profile beyond a candidate's own window
-//     is already feasible (every earlier admission certified its window), so these are
-//     exactly the t' in [t+1, t_max(U + {i})] of Eq. 5.  Admission adds the ramp s + tau
-//     (Eq. 3); advancing the clock is a one-lane shuffle.
-//   * the waiting queue R^(t): a two-level bitmap over ranks in shared memory; rank =
-//     position in (o~, idx) order for MC-SF (Alg. 1 line "ascending order of predicted
-//     output length") or idx for MC-Benchmark (arrival order).  The ranks
-//     come from a warp bitonic sort of packed keys, done once per instance.
-//   * packed per-request words {o~:6 | idx:14 | s:6 | o:6} by rank, arrivals a by idx.
+//         Prof(t+tau) + s + tau <= M  for every tau in [1, w].
+//     With o~ >= o the profile beyond a candidate's own window is already feasible (every
+//     earlier admission certified its window), so these are exactly the t' in
+//     [t+1, t_max(U + {i})] of Eq. 5.  Admission adds the ramp s + tau (Eq. 3);
+//     advancing the clock is a shuffle.
+//   * the waiting queue R^(t): a bitmap over ranks, one 32-bit word per lane for up to
+//     1024 ranks (else a two-level bitmap in shared memory); rank = position in (o~, idx)
+//     order for MC-SF (Alg. 1 "ascending order of predicted output length") or idx
+//     for MC-Benchmark (arrival order).  MC-SF ranks come from a stable warp
+//     counting sort on o~ (<= 63), once per instance.
+//   * packed per-request words {o~:6 | idx:14 | s:6 | o:6} by rank, arrivals a by idx,
+//     and start rounds p by idx; completions and starts are written to HBM once, coalesced,
+//     when the instance ends, and TEL = sum (p + o - a) is reduced in that pass.
 // The admission loop walks the queue head in rank order and stops at the first failure
 // (Alg. 1 "Break the for loop"): the longest feasible prefix of Eq. 6.
 //
-// Rounds with an empty queue are not iterated: nothing can be admitted in them, so the
-// clock jumps to the next arrival and the skipped rounds' occupancy is read off the
-// profile (DESIGN "Exact fast paths").  With o~ > o (early completion) a request
-// leaves S before its projected window ends; those instances run the plain per-round
-// loop with the unused tail removed from the profile at completion (Eq. 5 sums over the
+// Exact fast paths (DESIGN "Exact fast paths"):
+//   * rounds with an empty queue are not iterated: the clock jumps to the next arrival and
+//     the skipped rounds' occupancy is read off the profile;
+//   * a queue head that fails Eq. 5 keeps failing -- and, by the break rule, blocks every
+//     other request -- until the profile has drained enough, a request that sorts before it
+//     arrives, or (o~ > o) a request completes early.  first_fit_offset() evaluates Eq. 5
+//     for the head at all of the next 64 rounds in one warp pass, and the loop advances
+//     straight to the first round at which something can change.  Every skipped round is a
+//     decision round whose outcome ("admit nothing") was evaluated, so decision_rounds,
+//     peak memory and all outputs equal the one-round-at-a-time loop's
+//     (SCHED_FLAG_PER_ROUND runs that loop instead).
+// With o~ > o (early completion) a request leaves S before its projected window
+// ends; its unused tail is removed from the profile at completion (Eq. 5 sums over the
 // requests still in progress).
 #pragma once
 #include "params.cuh"
 
+#ifndef KV_SMALL_MIN_BLOCKS
+#define KV_SMALL_MIN_BLOCKS 8
+#endif
+
 namespace kv {
 
 struct SmallSmem {
-    uint32_t *keys;      // [NP] packed words by rank
+    uint32_t *keys;      // [NP] packed words by rank (MC-Benchmark: rank = idx)
+    uint32_t *kidx;      // [NP] packed words by idx (MC-SF, before ranking)
     int *arr;            // [NP] a by idx
+    int *pst;            // [NP] start round p by idx, -1 = not started
     uint16_t *arank;     // [NP] rank of idx (MC-SF)
-    uint32_t *bm;        // [NP/32]
-    uint32_t *sm;        // [32]
+    uint32_t *bm;        // [NP/32] shared-memory queue words (NP > 1024)
+    uint32_t *sm;        // [32] queue summary (NP > 1024) / insert staging (NP <= 1024)
+    int *hist;           // [64] o~ histogram / running bucket offsets (MC-SF)
 };
 
 __host__ __device__ inline int small_warp_bytes(int NP)
 {
-    int b = NP * 4 + NP * 4 + NP * 2 + (NP / 32) * 4 + 32 * 4;
+    int b = NP * 18 + (NP / 32) * 4 + 32 * 4 + 64 * 4;
     return (b + 15) & ~15;
 }
 
+// ---------------------------------------------------------------------------------------
+// waiting queue, register version: lane l holds bitmap word l (ranks 32l .. 32l+31)
+// ---------------------------------------------------------------------------------------
+struct RegQueue {
+    uint32_t word;
+    uint32_t *stage;     // [32] shared staging words for inserts
+
+    __device__ __forceinline__ void init(uint32_t *st, uint32_t *, int)
+    {
+        stage = st;
+        word = 0u;
+        stage[lane_id()] = 0u;
+        __syncwarp();
+    }
+    __device__ __forceinline__ void insert(bool take, int r)
+    {
+        if (take) atomicOr(&stage[r >> 5], 1u << (r & 31));
+    }
+    __device__ __forceinline__ void flush()
+    {
+        __syncwarp();
+        word |= stage[lane_id()];
+        stage[lane_id()] = 0u;
+        __syncwarp();
+    }
+    __device__ __forceinline__ int first() const
+    {
+        const uint32_t b = __ballot_sync(KV_FULL, word != 0u);
+        if (b == 0u) return KV_INF;
+        const int l0 = __ffs(b) - 1;
+        return (l0 << 5) + __ffs(__shfl_sync(KV_FULL, word, l0)) - 1;
+    }
+    __device__ __forceinline__ int pop(int h)
+    {
+        if (lane_id() == (h >> 5)) word &= ~(1u << (h & 31));
+        return first();
+    }
+};
+
+// waiting queue, shared-memory version (two-level bitmap, up to 32768 ranks)
+struct SmemQueue {
+    WarpQueue q;
+
+    __device__ __forceinline__ void init(uint32_t *sm, uint32_t *bm, int nw)
+    {
+        for (int w = lane_id(); w < nw; w += 32) bm[w] = 0u;
+        sm[lane_id()] = 0u;
+        __syncwarp();
+        q = WarpQueue{bm, sm, (nw + 31) >> 5};
+    }
+    __device__ __forceinline__ void insert(bool take, int r)
+    {
+        if (take) q_insert(q, r);
+    }
+    __device__ __forceinline__ void flush() { __syncwarp(); }
+    __device__ __forceinline__ int first() const { return q_first(q); }
+    __device__ __forceinline__ int pop(int h) { return q_pop_head(q, h); }
+};
+
+// ---------------------------------------------------------------------------------------
+// register profile helpers
+// ---------------------------------------------------------------------------------------
 // shift the register profile so that tau' = tau - d (d >= 1)
 __device__ __forceinline__ void prof_shift(int &P0, int &P1, int d)
 {
@@ -75,33 +155,36 @@ __device__ __forceinline__ int prof_max(int P0, int P1, int d)
     return warp_max_i32(v);
 }
 
-// Bit D (0 <= D < 64) of the result is set iff a head candidate (s, w) would violate
-// Eq. 5 at round t+D while the profile only advances (no admission, arrival or early
-// completion in between).  Position u = t+D+tau of the profile rules out the offsets
-// D in [u-w, u-1] with Prof(u) + s + (u - D) > M, i.e. D <= Prof(u) + u - (M-s) - 1; the
-// union over the 64 positions held by the warp is two OR-reductions.  Prof is zero
-// beyond tau = 63 (o~ <= 63), so the head always fits by D = 64.
-__device__ __forceinline__ unsigned long long blocked_rounds(int P0, int P1, int s, int w, int M)
+// First round offset D >= 0 at which a head candidate (s, w) satisfies Eq. 5 while the
+// profile only advances (no admission, arrival or early completion in between).  Profile
+// position u = D + tau (tau in [1, w]) rules out the offsets D in [u-w, u-1] for which
+// Prof(u) + s + (u - D) > M, i.e. D <= Prof(u) + u - (M-s) - 1: an interval.  The union
+// of the intervals of the 64 positions the warp holds is an OR-reduction of bit masks,
+// and the answer is its first zero bit.  Offsets 0..31 are resolved first (one 32-bit
+// reduction); 32..63 only when all of those are blocked.  Prof is zero beyond tau = 63
+// (o~ <= 63), so the head fits by D = 64 at the latest.
+__device__ __forceinline__ unsigned interval_bits(int lo, int hi, int base)
+{
+    lo = max(lo - base, 0);
+    hi = min(hi - base, 31);
+    return hi >= lo ? (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo) : 0u;
+}
+
+__device__ __forceinline__ int first_fit_offset(int P0, int P1, int s, int w, int M)
 {
     const int lane = lane_id();
     const int room = M - s;
-    unsigned long long m = 0ull;
-    {
-        const int u = lane + 1;
-        const int lo = max(0, u - w), hi = min(u - 1, P0 + u - room - 1);
-        if (hi >= lo) m |= (~0ull >> (63 - hi)) & (~0ull << lo);
-    }
-    {
-        const int u = lane + 33;
-        const int lo = max(0, u - w), hi = min(u - 1, P1 + u - room - 1);
-        if (hi >= lo) m |= (~0ull >> (63 - hi)) & (~0ull << lo);
-    }
-    const unsigned lo32 = __reduce_or_sync(KV_FULL, (unsigned)m);
-    const unsigned hi32 = __reduce_or_sync(KV_FULL, (unsigned)(m >> 32));
-    return ((unsigned long long)hi32 << 32) | lo32;
+    const int u0 = lane + 1, u1 = lane + 33;
+    const int lo0 = u0 - w, hi0 = min(u0 - 1, P0 + u0 - room - 1);
+    const int lo1 = u1 - w, hi1 = min(u1 - 1, P1 + u1 - room - 1);
+    const unsigned c0 = __reduce_or_sync(KV_FULL, interval_bits(lo0, hi0, 0) | interval_bits(lo1, hi1, 0));
+    if (c0 != 0xffffffffu) return __ffs(~c0) - 1;
+    const unsigned c1 = __reduce_or_sync(KV_FULL, interval_bits(lo0, hi0, 32) | interval_bits(lo1, hi1, 32));
+    return c1 != 0xffffffffu ? 32 + __ffs(~c1) - 1 : 64;
 }
 
-template <int POL, bool MULTI>
+// ---------------------------------------------------------------------------------------
+template <int POL, bool MULTI, class Queue>
 __device__ void small_instance(const KParams &P, long long inst, const SmallSmem &S)
 {
     const int lane = lane_id();
@@ -118,27 +201,24 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     }
 
     // ---- stage + validate (one coalesced 16-byte load per request) ------------------
-    const int NPi = next_pow2(max(n, 32));
     bool bad = false, slow = false;
     long long suma = 0, sumo = 0;
-    for (int k = lane; k < NPi; k += 32) {
-        uint32_t key = 0xffffffffu;
-        if (k < n) {
-            const int4 r = P.req[off + k];               // {a, s, o, o~}
-            bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
-            if (POL == POL_MCSF) {
-                bad |= r.y + r.w > M || r.w < r.z;        // DESIGN Q8; o~ >= o
-                slow |= r.w != r.z;
-            } else {
-                bad |= r.y + r.z > M;
-            }
-            suma += r.x;
-            sumo += r.z;
-            S.arr[k] = r.x;
-            const uint32_t w = (POL == POL_MCSF) ? (uint32_t)r.w : 0u;
-            key = (w << 26) | ((uint32_t)k << 12) | (((uint32_t)r.y & 63u) << 6) | ((uint32_t)r.z & 63u);
+    for (int k = lane; k < n; k += 32) {
+        const int4 r = P.req[off + k];                   // {a, s, o, o~}
+        bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
+        if (POL == POL_MCSF) {
+            bad |= r.y + r.w > M || r.w < r.z;            // DESIGN Q8; o~ >= o
+            slow |= r.w != r.z;
+        } else {
+            bad |= r.y + r.z > M;
         }
-        S.keys[k] = key;
+        suma += r.x;
+        sumo += r.z;
+        S.arr[k] = r.x;
+        S.pst[k] = -1;
+        const uint32_t w = (POL == POL_MCSF) ? (uint32_t)r.w : 0u;
+        const uint32_t key = (w << 26) | ((uint32_t)k << 12) | (((uint32_t)r.y & 63u) << 6) | ((uint32_t)r.z & 63u);
+        if (POL == POL_MCSF) S.kidx[k] = key; else S.keys[k] = key;
     }
     __syncwarp();
     for (int k = lane + 1; k < n; k += 32) bad |= S.arr[k] < S.arr[k - 1];
@@ -157,27 +237,47 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
         return;
     }
 
-    // ---- MC-SF: sort packed keys by (o~, idx) -> ranks (warp bitonic, once) ----------
+    // ---- MC-SF: ranks in (o~, idx) order by a stable counting sort on o~ <= 63 -----------
+    //   rank_i = #{j : o~_j < o~_i} + #{j < i : o~_j = o~_i}
     if (POL == POL_MCSF) {
-        for (int k = 2; k <= NPi; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < (NPi >> 1); i += 32) {
-                    const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-                    const int hi = lo + j;
-                    const bool up = (lo & k) == 0;
-                    const uint32_t x = S.keys[lo], y = S.keys[hi];
-                    if ((x > y) == up) { S.keys[lo] = y; S.keys[hi] = x; }
-                }
-                __syncwarp();
-            }
+        S.hist[lane] = 0;
+        S.hist[lane + 32] = 0;
+        __syncwarp();
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            const int v = k < n ? (int)(S.kidx[k] >> 26) : 64 + lane;
+            const unsigned peers = __match_any_sync(KV_FULL, v);
+            if (k < n && __ffs(peers) - 1 == lane) S.hist[v] += __popc(peers);
+            __syncwarp();
         }
-        for (int r = lane; r < n; r += 32) S.arank[(S.keys[r] >> 12) & 0x3fffu] = (uint16_t)r;
+        const int h0 = S.hist[2 * lane], h1 = S.hist[2 * lane + 1];
+        int x = h0 + h1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(KV_FULL, x, d);
+            if (lane >= d) x += y;
+        }
+        __syncwarp();
+        S.hist[2 * lane] = x - h0 - h1;
+        S.hist[2 * lane + 1] = x - h1;
+        __syncwarp();
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            const uint32_t key = k < n ? S.kidx[k] : 0u;
+            const int v = k < n ? (int)(key >> 26) : 64 + lane;
+            const unsigned peers = __match_any_sync(KV_FULL, v);
+            if (k < n) {
+                const int r = S.hist[v] + __popc(peers & ((1u << lane) - 1u));
+                S.keys[r] = key;
+                S.arank[k] = (uint16_t)r;
+            }
+            __syncwarp();
+            if (k < n && __ffs(peers) - 1 == lane) S.hist[v] += __popc(peers);
+            __syncwarp();
+        }
     }
-    const int nw = (NPi + 31) >> 5;
-    for (int w = lane; w < nw; w += 32) S.bm[w] = 0u;
-    S.sm[lane] = 0u;
-    __syncwarp();
-    WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
+    Queue Q;
+    Q.init(S.sm, S.bm, (next_pow2(max(n, 32)) + 31) >> 5);
 
     const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(S.arr[n - 1], sumo);
     const int cap = (int)min(cap64, 0x7ffffffell);
@@ -188,8 +288,8 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     int h = KV_INF;                  // queue head (rank), KV_INF = R empty
     uint32_t hkey = 0u;
     bool hstale = false;
+    bool head_fits = false;          // the head's first-fit round was computed and reached
     int P0 = 0, P1 = 0;              // Prof(t+lane+1), Prof(t+lane+33)
-    long long sumc = 0;
     int rounds = 0, drounds = 0;
     int maxc = -1, peak = 0, status = ST_OK;
     // early-completion records (slow mode): one lane per in-flight request with o~ > o
@@ -222,22 +322,21 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
         if (t > cap) { status = ST_LIVELOCK; break; }
 
         // arrivals a_i <= t join R^(t)
-        while (a_next <= t) {
-            const int k = next + lane;
-            const int ak = k < n ? S.arr[k] : KV_INF;
-            const bool take = ak <= t;
-            const int cnt = __popc(__ballot_sync(KV_FULL, take));
-            int rk = KV_INF;
-            if (take) {
-                rk = (POL == POL_MCSF) ? (int)S.arank[k] : k;
-                q_insert(Q, rk);
-            }
-            const int mn = warp_min_i32(rk);
-            if (mn < h) { h = mn; hstale = true; }
-            next += cnt;
-            a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? S.arr[next] : KV_INF);
+        if (a_next <= t) {
+            do {
+                const int k = next + lane;
+                const int ak = k < n ? S.arr[k] : KV_INF;
+                const bool take = ak <= t;
+                const int cnt = __popc(__ballot_sync(KV_FULL, take));
+                const int rk = take ? ((POL == POL_MCSF) ? (int)S.arank[k] : k) : KV_INF;
+                Q.insert(take, rk);
+                const int mn = warp_min_i32(rk);
+                if (mn < h) { h = mn; hstale = true; head_fits = false; }
+                next += cnt;
+                a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? S.arr[next] : KV_INF);
+            } while (a_next <= t);
+            Q.flush();
         }
-        __syncwarp();
 
         // early completions (o~ > o): drop the unused projected tail (slow mode only)
         if (slow) {
@@ -261,20 +360,18 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
         }
 
         // decision round t with R non-empty (Alg. 1 / Alg. 2): candidates in rank order,
-        // break at the first failure.  The failing head keeps failing -- and nothing else
-        // is admitted -- until it fits, a request arrives or (o~ > o) a request completes
-        // early; the coverage test finds the first of those rounds in one pass.
+        // break at the first failure.
         if (hstale) { hkey = S.keys[h]; hstale = false; }
         int jump = 1;
         for (;;) {
             const int w = (POL == POL_MCSF) ? (int)(hkey >> 26) : (int)(hkey & 63u);
             const int s = (int)((hkey >> 6) & 63u), o = (int)(hkey & 63u);
             if (MULTI) {
-                const unsigned long long cov = blocked_rounds(P0, P1, s, w, M);
-                if (cov & 1ull) {                                        // Eq. 5 violated now
-                    jump = (~cov == 0ull) ? 64 : __ffsll((long long)~cov) - 1;
-                    break;
+                if (!head_fits) {
+                    const int d = first_fit_offset(P0, P1, s, w, M);
+                    if (d > 0) { jump = d; break; }                      // Eq. 5 violated now
                 }
+                head_fits = false;
             } else {
                 const int tau0 = lane + 1, tau1 = lane + 33;
                 const bool v = (tau0 <= w && P0 + s + tau0 > M) || (tau1 <= w && P1 + s + tau1 > M);
@@ -282,26 +379,35 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
             }
             if (lane + 1 <= w) P0 += s + lane + 1;                       // ramp s + tau (Eq. 3)
             if (lane + 33 <= w) P1 += s + lane + 33;
-            const int idx = (int)((hkey >> 12) & 0x3fffu);
-            const int c = t + o;                                         // c_i = p_i + o_i
-            if (lane == 0) {
-                if (P.completion) P.completion[off + idx] = c;
-                if (P.start) P.start[off + idx] = t;
-            }
-            sumc += c;
-            maxc = max(maxc, c);
+            if (lane == 0) S.pst[(hkey >> 12) & 0x3fffu] = t;            // p_i = t
+            maxc = max(maxc, t + o);                                     // c_i = p_i + o_i
             if (POL == POL_MCSF && w > o) {                               // early completion
                 const uint32_t fr = __ballot_sync(KV_FULL, rc == KV_INF);
-                if (lane == __ffs(fr) - 1) { rc = c; rs = s; rp = t; rw = w; }
+                if (lane == __ffs(fr) - 1) { rc = t + o; rs = s; rp = t; rw = w; }
             }
-            h = q_pop_head(Q, h);
+            h = Q.pop(h);
             if (h == KV_INF) break;
             hkey = S.keys[h];
         }
         if (MULTI && jump > 1) {
-            jump = min(jump, a_next - t);                 // a new request may become the head
-            jump = min(jump, cap + 1 - t);
-            if (slow) jump = min(jump, warp_min_i32(rc) - t);
+            int T = t + min(jump, cap + 1 - t);
+            if (slow) T = min(T, warp_min_i32(rc));
+            // an arrival before T ends the jump only if it becomes the new head, i.e. its
+            // key (o~, idx) precedes the blocked head's; in arrival order (MC-Benchmark) a
+            // newcomer never does.  Other arrivals join R at the landing round (no decision
+            // is taken in between, so when exactly they join does not matter).
+            if (POL == POL_MCSF) {
+                for (int k = next; a_next < T && k < n; k += 32) {
+                    const int kk = k + lane;
+                    const int ak = kk < n ? S.arr[kk] : KV_INF;
+                    const bool before = ak < T;
+                    const uint32_t m = __ballot_sync(KV_FULL, before && (int)S.arank[min(kk, n - 1)] < h);
+                    if (m) { T = __shfl_sync(KV_FULL, ak, __ffs(m) - 1); break; }
+                    if (!__all_sync(KV_FULL, before)) break;
+                }
+            }
+            head_fits = T == t + jump;        // landing where the unchanged head fits
+            jump = T - t;
         }
         // rounds t .. t+jump-1: decision rounds (R non-empty), batch memory Prof(t+1..t+jump)
         drounds += jump;
@@ -316,23 +422,18 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
         t += jump;
     }
 
-    if (status != ST_OK) {
-        // requests never started (still waiting, or not yet arrived) report -1
-        for (int k = next + lane; k < n; k += 32) {
-            if (P.completion) P.completion[off + k] = -1;
-            if (P.start) P.start[off + k] = -1;
-        }
-        for (int w = lane; w < nw; w += 32) {
-            uint32_t bits = S.bm[w];
-            while (bits) {
-                const int r = (w << 5) + __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int idx = (POL == POL_MCSF) ? (int)((S.keys[r] >> 12) & 0x3fffu) : r;
-                if (P.completion) P.completion[off + idx] = -1;
-                if (P.start) P.start[off + idx] = -1;
-            }
-        }
+    // ---- outputs: coalesced completion / start, TEL ------------------------------
+    __syncwarp();
+    long long sumc = 0;
+    for (int k = lane; k < n; k += 32) {
+        const int p = S.pst[k];
+        const uint32_t key = (POL == POL_MCSF) ? S.kidx[k] : S.keys[k];
+        const int c = p < 0 ? -1 : p + (int)(key & 63u);
+        sumc += c;
+        if (P.completion) P.completion[off + k] = c;
+        if (P.start) P.start[off + k] = p;
     }
+    sumc = warp_sum_i64(sumc);
     res.tel = sumc - suma;
     res.rounds = rounds;
     res.decision_rounds = drounds;
@@ -342,8 +443,8 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     write_result(P, inst, res);
 }
 
-template <int POL, bool MULTI>
-__global__ void __launch_bounds__(128) k_mc_small(const KParams P)
+template <int POL, bool MULTI, bool QREG>
+__global__ void __launch_bounds__(128, KV_SMALL_MIN_BLOCKS) k_mc_small(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -351,18 +452,22 @@ __global__ void __launch_bounds__(128) k_mc_small(const KParams P)
     const int NP = P.NP;
     SmallSmem S;
     S.keys = reinterpret_cast<uint32_t *>(base);
-    S.arr = reinterpret_cast<int *>(base + NP * 4);
-    S.arank = reinterpret_cast<uint16_t *>(base + NP * 8);
-    S.bm = reinterpret_cast<uint32_t *>(base + NP * 10);
-    S.sm = reinterpret_cast<uint32_t *>(base + NP * 10 + (NP / 32) * 4);
+    S.kidx = reinterpret_cast<uint32_t *>(base + NP * 4);
+    S.arr = reinterpret_cast<int *>(base + NP * 8);
+    S.pst = reinterpret_cast<int *>(base + NP * 12);
+    S.arank = reinterpret_cast<uint16_t *>(base + NP * 16);
+    S.bm = reinterpret_cast<uint32_t *>(base + NP * 18);
+    S.sm = reinterpret_cast<uint32_t *>(base + NP * 18 + (NP / 32) * 4);
+    S.hist = reinterpret_cast<int *>(base + NP * 18 + (NP / 32) * 4 + 128);
 
     long long inst = 0;
-    if (lane == 0) inst = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
+    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
     inst = __shfl_sync(KV_FULL, inst, 0);
     while (inst < P.n_inst) {
         long long nxt = 0;     // claim the next instance now; the latency hides behind this one
-        if (lane == 0) nxt = atomicAdd(reinterpret_cast<unsigned long long *>(P.counter), 1ull);
-        small_instance<POL, MULTI>(P, inst, S);
+        if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
+        if (QREG) small_instance<POL, MULTI, RegQueue>(P, inst, S);
+        else small_instance<POL, MULTI, SmemQueue>(P, inst, S);
         inst = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();
     }

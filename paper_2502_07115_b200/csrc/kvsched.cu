@@ -159,23 +159,35 @@ __global__ void k_philox(long long n, const uint4 *ctr, const uint2 *key, uint4 
 }
 
 template <typename K>
-int occupancy_grid(sched_ctx *c, K kernel, int smem, long long work_warps, int *grid)
+int occupancy_grid(sched_ctx *c, K kernel, int block, int smem, long long work_warps, int *grid)
 {
     int per_sm = 0;
-    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
+    CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
     if (per_sm < 1) return fail(c, SCHED_E_ARG, "kernel does not fit one block per SM (smem %d B)", smem);
-    long long blocks = (work_warps + (kBlock / 32) - 1) / (kBlock / 32);
+    long long blocks = (work_warps + (block / 32) - 1) / (block / 32);
     long long cap = (long long)per_sm * c->num_sms;
     *grid = (int)(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
     return SCHED_OK;
 }
 
-template <typename K>
-int launch_sim(sched_ctx *c, K kernel, const KParams &P, int smem, const char *name)
+// warps per block (1..4) such that the per-warp shared memory fits one block
+int warps_per_block(const sched_ctx *c, int warp_bytes)
 {
+    int w = kBlock / 32;
+    while (w > 1 && (size_t)w * warp_bytes > c->max_smem_optin) --w;
+    return w;
+}
+
+template <typename K>
+int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const char *name)
+{
+    const int wpb = warps_per_block(c, warp_bytes);
+    const int block = 32 * wpb, smem = warp_bytes * wpb;
+    if ((size_t)smem > c->max_smem_optin)
+        return fail(c, SCHED_E_ARG, "%s needs %d B shared memory per warp", name, warp_bytes);
     CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int grid = 1;
-    int rc = occupancy_grid(c, kernel, smem, P.n_inst, &grid);
+    int rc = occupancy_grid(c, kernel, block, smem, P.n_inst, &grid);
     if (rc) return rc;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
@@ -183,7 +195,7 @@ int launch_sim(sched_ctx *c, K kernel, const KParams &P, int smem, const char *n
         e1 = take_event(c);
         CUDA_TRY(c, cudaEventRecord(e0, c->stream));
     }
-    kernel<<<grid, kBlock, smem, c->stream>>>(P);
+    kernel<<<grid, block, smem, c->stream>>>(P);
     CUDA_TRY(c, cudaGetLastError());
     if (c->timing) {
         CUDA_TRY(c, cudaEventRecord(e1, c->stream));
@@ -336,27 +348,35 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
 
     const bool mc = pol->policy == SCHED_MCSF || pol->policy == SCHED_MC_BENCH;
-    if (mc && max_mem <= kSmallMaxMem && max_req <= kSmallMaxRequests) {
-        P.NP = next_pow2(max_req < 32 ? 32 : max_req);
+    const int np_small = next_pow2(max_req < 32 ? 32 : max_req);
+    if (mc && max_mem <= kSmallMaxMem && max_req <= kSmallMaxRequests &&
+        (size_t)small_warp_bytes(np_small) <= c->max_smem_optin) {
+        P.NP = np_small;
         P.warp_bytes = small_warp_bytes(P.NP);
-        const int smem = P.warp_bytes * (kBlock / 32);
-        if ((size_t)smem > c->max_smem_optin)
-            return fail(c, SCHED_E_ARG, "small kernel needs %d B shared memory per block", smem);
+        const int smem = P.warp_bytes;
         const bool per_round = pol->flags & SCHED_FLAG_PER_ROUND;
-        if (pol->policy == SCHED_MCSF)
-            return per_round ? launch_sim(c, k_mc_small<POL_MCSF, false>, P, smem, "k_mc_small<MCSF,per-round>")
-                             : launch_sim(c, k_mc_small<POL_MCSF, true>, P, smem, "k_mc_small<MCSF>");
-        return per_round ? launch_sim(c, k_mc_small<POL_MCBENCH, false>, P, smem, "k_mc_small<MCBENCH,per-round>")
-                         : launch_sim(c, k_mc_small<POL_MCBENCH, true>, P, smem, "k_mc_small<MCBENCH>");
+        const bool qreg = P.NP <= 1024;          // waiting queue fits one word per lane
+#define KV_SMALL(POLV, MULTIV, QREGV, NAME) launch_sim(c, k_mc_small<POLV, MULTIV, QREGV>, P, smem, NAME)
+        if (pol->policy == SCHED_MCSF) {
+            if (per_round) return qreg ? KV_SMALL(POL_MCSF, false, true, "k_mc_small<MCSF,per-round>")
+                                       : KV_SMALL(POL_MCSF, false, false, "k_mc_small<MCSF,per-round,smemq>");
+            return qreg ? KV_SMALL(POL_MCSF, true, true, "k_mc_small<MCSF>")
+                        : KV_SMALL(POL_MCSF, true, false, "k_mc_small<MCSF,smemq>");
+        }
+        if (per_round) return qreg ? KV_SMALL(POL_MCBENCH, false, true, "k_mc_small<MCBENCH,per-round>")
+                                   : KV_SMALL(POL_MCBENCH, false, false, "k_mc_small<MCBENCH,per-round,smemq>");
+        return qreg ? KV_SMALL(POL_MCBENCH, true, true, "k_mc_small<MCBENCH>")
+                    : KV_SMALL(POL_MCBENCH, true, false, "k_mc_small<MCBENCH,smemq>");
+#undef KV_SMALL
     }
 
     // ring kernel: profile ring L > max_len (and > M - 1 for the projection window)
     P.NP = next_pow2(max_req < 32 ? 32 : max_req);
     P.L = next_pow2(max_len + 1);
     P.warp_bytes = ring_warp_bytes(P.L, P.NP, pol->policy);
-    const int smem = P.warp_bytes * (kBlock / 32);
+    const int smem = P.warp_bytes;
     if ((size_t)smem > c->max_smem_optin)
-        return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per block (L=%d, NP=%d)", smem, P.L, P.NP);
+        return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)", smem, P.L, P.NP);
     const size_t slots = (size_t)inst->n_instances * (size_t)max_req;
     if (pol->policy == SCHED_MCSF) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;

@@ -59,10 +59,12 @@ def load() -> ctypes.CDLL:
     """Load the in-tree library (raises if it was not built)."""
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
-            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+        import os
+        path = Path(os.environ.get("KVSCHED_LIB", LIB_PATH))   # experiments only
+        if not path.exists():
+            raise RuntimeError(f"{path} is missing: run __graft_entry__.build() "
                                "(there is no CPU fallback)")
-        L = ctypes.CDLL(str(LIB_PATH))
+        L = ctypes.CDLL(str(path))
         L.sched_abi_version.restype = ctypes.c_int
         L.sched_init.argtypes = [ctypes.POINTER(P), ctypes.c_int, P]
         L.sched_set_stream.argtypes = [P, P]

@@ -129,6 +129,17 @@ def test_per_round_and_multi_round_modes(K, ctx, oracle_mod, maker, pol):
         check(K, ctx, oracle_mod, b, pol, f"{maker} flags={flags}", flags=flags, **kw)
 
 
+@pytest.mark.parametrize("pol", [0, 1])
+def test_small_kernel_large_queues(K, ctx, oracle_mod, pol):
+    """More than 1024 requests per instance with M <= 64: the fused kernel keeps the waiting
+    queue as a two-level shared-memory bitmap instead of one word per lane."""
+    b = W.am1(6, 37, n=3000, M=48)
+    for flags in (0, 1):
+        check(K, ctx, oracle_mod, b, pol, f"n=3000 flags={flags}", flags=flags)
+    c = W.random_small(60, 38, n_max=2500, M_lo=20, M_hi=64, a_max=3000)
+    check(K, ctx, oracle_mod, c, pol, "ragged large n")
+
+
 def test_am1_paper_draw(K, ctx, oracle_mod):
     b = W.am1_paper(400, 14)
     check(K, ctx, oracle_mod, b, 0, "AM1-paper")

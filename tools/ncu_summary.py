@@ -1,0 +1,104 @@
+#!/usr/bin/env python
+"""Summarise an ncu --set full capture: key metrics per kernel, the hottest SASS, and
+(optionally) merge per-launch DRAM traffic into profiles/ncu_summary.json (read by bench.py).
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--json profiles/ncu_summary.json] [--top 30]
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import re
+import subprocess
+from pathlib import Path
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.per_cycle_active",
+    "smsp__warps_eligible.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__inst_executed.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__cycles_elapsed.avg", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+]
+
+
+def ncu(*args) -> str:
+    return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
+
+
+def raw(rep: str) -> list[dict]:
+    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        d["_units"] = dict(zip(hdr, units))
+        out.append(d)
+    return out
+
+
+def to_bytes(v: str, unit: str) -> float:
+    x = float(v.replace(",", ""))
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def to_ns(v: str, unit: str) -> float:
+    x = float(v.replace(",", ""))
+    return x * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(unit, 1)
+
+
+def hot_sass(rep: str, top: int):
+    text = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass")
+    rows = list(csv.reader(io.StringIO(text)))
+    if len(rows) < 3:
+        return [], 0
+    hdr = rows[1]
+    ia, isrc = hdr.index("Instructions Executed"), hdr.index("Source")
+    ist = hdr.index("Warp Stall Sampling (All Samples)")
+    data = [(int(r[ia] or 0), int(r[ist] or 0), r[isrc].strip()) for r in rows[2:] if len(r) > ist]
+    tot = sum(d[0] for d in data)
+    return sorted(data, key=lambda x: -x[1])[:top], tot
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--json")
+    ap.add_argument("--top", type=int, default=25)
+    a = ap.parse_args()
+    kernels = {}
+    for d in raw(a.rep):
+        name = d.get("Kernel Name", "?")
+        short = re.sub(r"\(.*", "", name).replace("void ", "").replace("kv::", "")
+        u = d["_units"]
+        rd = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
+        wr = to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+        dur = to_ns(d["gpu__time_duration.sum"], u["gpu__time_duration.sum"])
+        print(f"== {short}")
+        for m in METRICS:
+            if m in d:
+                print(f"  {m:70s} {d[m]:>16s} {u.get(m, '')}")
+        print(f"  dram bytes per launch: {rd + wr:.4g}  duration {dur / 1e6:.4f} ms")
+        kernels[short] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                          "duration_ms": dur / 1e6, "source": Path(a.rep).name,
+                          "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                          "registers": d.get("launch__registers_per_thread"),
+                          "warp_inst": d.get("smsp__inst_executed.sum")}
+    hot, tot = hot_sass(a.rep, a.top)
+    print(f"== hottest SASS by stall samples (total warp instructions {tot:.4g})")
+    for c, s, src in hot:
+        print(f"  {c:12d} {s:7d}  {src[:90]}")
+    if a.json:
+        p = Path(a.json)
+        cur = json.loads(p.read_text()) if p.exists() else {"kernels": {}}
+        cur.setdefault("kernels", {}).update(kernels)
+        cur["note"] = ("dram bytes per launch from ncu --set full --clock-control none (one launch per "
+                       "kernel, cold cache, replayed); see the .txt summaries beside this file")
+        p.write_text(json.dumps(cur, indent=1))
+
+
+if __name__ == "__main__":
+    main()
