@@ -76,7 +76,7 @@ def make_workload(name: str, n: int, rank: int):
 
 def policy_of(K, name):
     if name == "alpha":
-        return K.Policy("alpha", (3, 10))
+        return K.Policy("alpha", (1, 4))
     if name == "alpha_beta":
         return K.Policy("alpha_beta", (1, 5), W.beta_threshold(0.1), seed=1)
     return K.Policy(name)
@@ -85,7 +85,7 @@ def policy_of(K, name):
 def oracle_policy(name):
     import oracle
     return {"mcsf": (oracle.MCSF, {}), "mcbench": (oracle.MCBENCH, {}),
-            "alpha": (oracle.ALPHA, dict(alpha=(3, 10))),
+            "alpha": (oracle.ALPHA, dict(alpha=(1, 4))),
             "alpha_beta": (oracle.ALPHA_BETA, dict(alpha=(1, 5), beta_thresh=W.beta_threshold(0.1), seed=1))}[name]
 
 

@@ -213,6 +213,8 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
 
         int64_t nR = 0, nS = 0, next = 0;
         int64_t t = a[0];
+        /* alpha-greedy cycle detection (DESIGN Q24): state at the last clear-all */
+        int64_t have_clear = 0, next_at_clear = 0, completed_since_clear = 0;
         /* "for each round t" */
         while (next < n || nR > 0 || nS > 0) {
             if (nR == 0 && nS == 0) t = a[next];           /* idle: jump to next arrival */
@@ -225,7 +227,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
             }
             /* release: j completes at c_j = p_j + o_j; its KV cache clears */
             for (int64_t k = 0; k < nS;) {
-                if (c[S[k]] <= t) or_remove_at(S, &nS, k); else k++;
+                if (c[S[k]] <= t) { or_remove_at(S, &nS, k); completed_since_clear++; } else k++;
             }
             if (nR > 0) decision_rounds++;
 
@@ -286,6 +288,17 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                             evictions++;
                         }
                         nS = 0;
+                        /* "infinite processing loops": after a clear-all the state is
+                         * (S empty, R, zero memory).  If nothing completed and nothing arrived
+                         * since the previous clear-all, R is the same set as then, and the
+                         * deterministic run from here repeats the last cycle for ever.      */
+                        if (have_clear && next == next_at_clear && completed_since_clear == 0) {
+                            status = OR_LIVELOCK;
+                            break;
+                        }
+                        have_clear = 1;
+                        next_at_clear = next;
+                        completed_since_clear = 0;
                     } else {
                         /* "each active request is cleared and sent back to the scheduler
                          * with an independent probability beta", in whole passes

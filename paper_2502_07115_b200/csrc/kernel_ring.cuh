@@ -2,17 +2,22 @@
 //
 // Same round structure as kernel_small.cuh, but the memory profile is a ring of L int32
 // slots in shared memory (slot r & (L-1) holds absolute round r, L a power of two larger
-// than every request length), so a candidate's Eq. 5 test and its admission are
-// ceil(w/32) warp-wide passes over its own window.  Per-request data stay in HBM/L2 and
-// are fetched when a request reaches the head of the queue.
+// than every request length + 32), so a candidate's Eq. 5 test and its admission
+// are ceil(w/32) warp-wide passes over its own window.  Per-request data stay in HBM/L2
+// and are fetched when a request reaches the head of the queue.
 //
 //   MC-SF / MC-Benchmark : ring = projected memory of S (Eq. 5 LHS), as in the small kernel.
+//                           A blocked head is resolved over the next 32 rounds per pass
+//                           (ring_first_fit), arrivals end the jump only if they sort before
+//                           the head.
 //   alpha / alpha-beta    : ring = actual memory (Eq. 3, true o).  Admission is FCFS with
 //                           threshold B = floor((1-alpha)M) on the next-round occupancy
 //                           (DESIGN Q12); when Mem(t+1) > M the active set is cleared
 //                            or thinned by independent Philox draws (DESIGN Q14).
-//                           The in-flight set is a bitmap over idx (plus start rounds in
-//                           global scratch) walked only on overflow.
+//                           Rounds in which nothing can happen (head over threshold, no
+//                           overflow, no arrival into an empty queue) are found 32 at a time
+//                           by one ballot over the ring.  The in-flight set is a bitmap over
+//                           idx (plus start rounds in global scratch) walked only on overflow.
 #pragma once
 #include "params.cuh"
 
@@ -30,20 +35,6 @@ __host__ __device__ inline int ring_warp_bytes(int L, int NP, int policy)
     int b = L * 4 + (NP / 32) * 4 + 32 * 4;
     if (policy >= POL_ALPHA) b += (NP / 32) * 4;
     return (b + 15) & ~15;
-}
-
-// Eq. 5 for one candidate: Prof(t+tau) + s + tau <= M for tau in [1, w]
-__device__ __forceinline__ bool ring_fits(const int *prof, int mask, int t, int s, int w, long long M)
-{
-    const int lane = lane_id();
-    for (int base = 1; base <= w; base += 64) {
-        const int ta = base + lane, tb = base + 32 + lane;
-        const int va = ta <= w ? prof[(t + ta) & mask] : 0;
-        const int vb = tb <= w ? prof[(t + tb) & mask] : 0;
-        const bool bad = (ta <= w && (long long)va + s + ta > M) || (tb <= w && (long long)vb + s + tb > M);
-        if (__any_sync(KV_FULL, bad)) return false;
-    }
-    return true;
 }
 
 // Prof(t+tau) += sign * (base + tau) for tau in [1, e]
@@ -64,6 +55,26 @@ __device__ __forceinline__ int ring_max_zero(int *prof, int mask, int t, int d, 
     }
     __syncwarp();
     return warp_max_i32(v);
+}
+
+// First offset D in [0, 31] at which the head (s, w) satisfies Eq. 5 while the ring only
+// advances; 32 if it is blocked at all of them.  Ring position u = D + tau rules out the
+// offsets D in [u-w, u-1] with Prof(u) + s + u - D > M (see first_fit_offset in
+// kernel_small.cuh); positions beyond w + 31 cannot reach D <= 31.
+__device__ __forceinline__ int ring_first_fit(const int *prof, int mask, int t, int s, int w, int M)
+{
+    const int lane = lane_id();
+    const int room = M - s;
+    unsigned cov = 0u;
+    for (int base = 1; base <= w + 31; base += 32) {
+        const int u = base + lane;
+        const int D = prof[(t + u) & mask];
+        const int lo = max(u - w, 0);
+        const int hi = min(min(u - 1, D + u - room - 1), 31);
+        if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
+    }
+    cov = __reduce_or_sync(KV_FULL, cov);
+    return cov == 0xffffffffu ? 32 : __ffs(~cov) - 1;
 }
 
 template <int POL>
@@ -120,18 +131,25 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     __syncwarp();
     WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
 
-    const long long cap = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
+    const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
+    const int cap = (int)min(cap64, 0x7ffffffell);
     const long long B = MC ? 0 : ((long long)(P.alpha_den - P.alpha_num) * M) / P.alpha_den;
     const unsigned long long gid = P.id0 + (unsigned long long)inst;
+    const bool multi = !(P.flags & 1);
 
     int t = reqi[off * 4];
     int next = 0, a_next = t;
     int h = KV_INF;
     uint4 he = make_uint4(0, 0, 0, 0);   // head entry {s, w, o, idx}
-    bool hstale = false;
-    long long sumc = 0, rounds = 0, drounds = 0, evictions = 0;
+    bool hstale = false, head_fits = false;
+    long long sumc = 0, evictions = 0;
+    int rounds = 0, drounds = 0;
     int maxc = -1, peak = 0, status = ST_OK;
     int mem_prev = 0;                    // alpha: Mem(t) of the previous round
+    // alpha-greedy cycle detection (DESIGN Q24): admissions since the last clear-all and the
+    // arrival pointer then; a clear-all that evicts everything admitted since the previous
+    // one (nothing completed) with no arrival in between repeats that cycle for ever.
+    int adm_since_clear = 0, next_at_clear = -1;
 
     auto fetch = [&](int r) -> uint4 {
         if (POL == POL_MCSF) return P.rq[off + r];
@@ -143,16 +161,16 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
         if (h == KV_INF) {
             if (MC) {
                 if (a_next == KV_INF) {                        // drain
-                    const long long E = min((long long)maxc, cap + 1);
-                    if (E > t) peak = max(peak, ring_max_zero(S.prof, mask, t, (int)min(E - t, (long long)L), 0));
+                    const int E = min(maxc, cap + 1);
+                    if (E > t) peak = max(peak, ring_max_zero(S.prof, mask, t, min(E - t, L), 0));
                     if (maxc > t) rounds += maxc - t;
-                    if ((long long)maxc >= cap + 1) status = ST_LIVELOCK;
+                    if (maxc >= cap + 1) status = ST_LIVELOCK;
                     break;
                 }
                 const int tn = a_next;
                 if (tn > t) {                                  // skip rounds t..tn-1
-                    const long long E = min((long long)tn, cap + 1);
-                    const int d = E > t ? (int)min(E - t, (long long)L) : 0;
+                    const int E = min(tn, cap + 1);
+                    const int d = E > t ? min(E - t, L) : 0;
                     peak = max(peak, ring_max_zero(S.prof, mask, t, d, min(tn - t, L)));
                     rounds += max(0, min(tn, maxc) - t);
                     if (tn > cap) { status = ST_LIVELOCK; break; }
@@ -177,132 +195,172 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 q_insert(Q, rk);
             }
             const int mn = warp_min_i32(rk);
-            if (mn < h) { h = mn; hstale = true; }
+            if (mn < h) { h = mn; hstale = true; head_fits = false; }
             next += cnt;
             a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? reqi[(off + next) * 4] : KV_INF);
         }
         __syncwarp();
 
         const bool had_R = h != KV_INF;
-        if (had_R) ++drounds;
         if (MC) {
-            if (had_R) {
-                if (hstale) { he = fetch(h); hstale = false; }
-                for (;;) {
-                    const int s = (int)he.x, w = (int)he.y, o = (int)he.z, idx = (int)he.w;
-                    if (!ring_fits(S.prof, mask, t, s, w, M)) break;
-                    ring_ramp(S.prof, mask, t, w, s, +1);
-                    const int c = t + o;
-                    if (lane == 0) {
-                        if (P.completion) P.completion[off + idx] = c;
-                        if (P.start) P.start[off + idx] = t;
+            // decision round t with R non-empty (Alg. 1 / Alg. 2)
+            if (hstale) { he = fetch(h); hstale = false; }
+            int jump = 1;
+            bool blocked_through = false;                 // head blocked at all 32 offsets
+            for (;;) {
+                const int s = (int)he.x, w = (int)he.y, o = (int)he.z, idx = (int)he.w;
+                if (!head_fits) {
+                    int d;
+                    if (multi) {
+                        d = ring_first_fit(S.prof, mask, t, s, w, M);
+                    } else {
+                        bool bad_ = false;
+                        for (int tau = lane + 1; tau <= w; tau += 32)
+                            bad_ |= S.prof[(t + tau) & mask] + s + tau > M;
+                        d = __any_sync(KV_FULL, bad_) ? 1 : 0;
                     }
-                    sumc += c;
-                    maxc = max(maxc, c);
-                    __syncwarp();
-                    h = q_pop_head(Q, h);
-                    if (h == KV_INF) break;
-                    he = fetch(h);
+                    if (d > 0) { jump = d; blocked_through = d == 32; break; }   // Eq. 5 violated
                 }
+                head_fits = false;
+                ring_ramp(S.prof, mask, t, w, s, +1);
+                const int c = t + o;
+                if (lane == 0) {
+                    if (P.completion) P.completion[off + idx] = c;
+                    if (P.start) P.start[off + idx] = t;
+                }
+                sumc += c;
+                maxc = max(maxc, c);
+                __syncwarp();
+                h = q_pop_head(Q, h);
+                if (h == KV_INF) break;
+                he = fetch(h);
             }
-            ++rounds;
-        } else {
-            const int occ = S.prof[(t + 1) & mask];           // Mem(t+1) of S
-            const bool idle_before = occ == 0;
-            long long Lnext = occ;
-            int admitted = 0;
-            if (had_R) {
-                if (hstale) { he = fetch(h); hstale = false; }
-                for (;;) {
-                    const int s = (int)he.x, o = (int)he.z, idx = (int)he.w;
-                    if (Lnext + s + 1 > B) break;                   // (1-alpha)M threshold
-                    Lnext += s + 1;
-                    ring_ramp(S.prof, mask, t, o, s, +1);
-                    const int c = t + o;
-                    if (lane == 0) {
-                        if (P.completion) P.completion[off + idx] = c;
-                        if (P.start) P.start[off + idx] = t;
-                        P.pstart[off + idx] = t;                            // start scratch
-                        S.infl[idx >> 5] |= 1u << (idx & 31);
+            if (jump > 1) {
+                int T = t + min(jump, cap + 1 - t);
+                if (POL == POL_MCSF) {
+                    // an arrival before T ends the jump only if it sorts before the head
+                    for (int k = next; a_next < T && k < n; k += 32) {
+                        const int kk = k + lane;
+                        const int ak = kk < n ? reqi[(off + kk) * 4] : KV_INF;
+                        const bool before = ak < T;
+                        const uint32_t m = __ballot_sync(KV_FULL, before && P.arank[off + min(kk, n - 1)] < h);
+                        if (m) { T = __shfl_sync(KV_FULL, ak, __ffs(m) - 1); break; }
+                        if (!__all_sync(KV_FULL, before)) break;
                     }
-                    sumc += c;
-                    ++admitted;
-                    __syncwarp();
-                    h = q_pop_head(Q, h);
-                    if (h == KV_INF) break;
-                    he = fetch(h);
                 }
+                head_fits = !blocked_through && T == t + jump;
+                jump = T - t;
             }
-            __syncwarp();
-            int mem = S.prof[(t + 1) & mask];
-            if (mem > M) {
-                // overflow of the batch of round t (DESIGN Q13): clear or thin
-                const int *pst = P.pstart;
-                for (int pass = 0;; ++pass) {
-                    int left = 0;
-                    for (int wb = 0; wb < nw; wb += 32) {
-                        const int wi = wb + lane;
-                        uint32_t bits = wi < nw ? S.infl[wi] : 0u;
-                        uint32_t keep = bits;
-                        while (__any_sync(KV_FULL, bits != 0u)) {
-                            int j = -1, pj = 0, sj = 0, oj = 0;
-                            bool ev = false, act = false;
-                            if (bits) {
-                                j = (wi << 5) + __ffs(bits) - 1;
-                                bits &= bits - 1;
-                                pj = pst[off + j];
-                                sj = reqi[(off + j) * 4 + 1];
-                                oj = reqi[(off + j) * 4 + 2];
-                                act = pj + oj > t;
-                                if (!act) keep &= ~(1u << (j & 31));   // completed earlier
-                                else {
-                                    ev = (POL == POL_ALPHA) ||
-                                         (unsigned long long)evict_draw(P.seed, gid, t, pass, j) < P.beta_thresh;
-                                    if (ev) keep &= ~(1u << (j & 31));
-                                }
+            drounds += jump;
+            rounds += jump;
+            peak = max(peak, ring_max_zero(S.prof, mask, t, jump, jump));
+            t += jump;
+            continue;
+        }
+
+        // ---- alpha / alpha-beta ----------------------------------------------------------
+        const int occ = S.prof[(t + 1) & mask];           // Mem(t+1) of S
+        const bool idle_before = occ == 0;
+        long long Lnext = occ;
+        int admitted = 0;
+        if (had_R) {
+            ++drounds;
+            if (hstale) { he = fetch(h); hstale = false; }
+            for (;;) {
+                const int s = (int)he.x, o = (int)he.z, idx = (int)he.w;
+                if (Lnext + s + 1 > B) break;                   // (1-alpha)M threshold
+                Lnext += s + 1;
+                ring_ramp(S.prof, mask, t, o, s, +1);
+                const int c = t + o;
+                if (lane == 0) {
+                    if (P.completion) P.completion[off + idx] = c;
+                    if (P.start) P.start[off + idx] = t;
+                    P.pstart[off + idx] = t;                            // start scratch
+                    S.infl[idx >> 5] |= 1u << (idx & 31);
+                }
+                sumc += c;
+                ++admitted;
+                ++adm_since_clear;
+                __syncwarp();
+                h = q_pop_head(Q, h);
+                if (h == KV_INF) break;
+                he = fetch(h);
+            }
+        }
+        __syncwarp();
+        int mem = S.prof[(t + 1) & mask];
+        bool cycle = false;
+        if (mem > M) {
+            // overflow of the batch of round t (DESIGN Q13): clear or thin
+            const int *pst = P.pstart;
+            const long long ev_before = evictions;
+            for (int pass = 0;; ++pass) {
+                int left = 0;
+                for (int wb = 0; wb < nw; wb += 32) {
+                    const int wi = wb + lane;
+                    uint32_t bits = wi < nw ? S.infl[wi] : 0u;
+                    uint32_t keep = bits;
+                    while (__any_sync(KV_FULL, bits != 0u)) {
+                        int j = -1, pj = 0, sj = 0, oj = 0;
+                        bool ev = false, act = false;
+                        if (bits) {
+                            j = (wi << 5) + __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            pj = pst[off + j];
+                            sj = reqi[(off + j) * 4 + 1];
+                            oj = reqi[(off + j) * 4 + 2];
+                            act = pj + oj > t;
+                            if (!act) keep &= ~(1u << (j & 31));   // completed earlier
+                            else {
+                                ev = (POL == POL_ALPHA) ||
+                                     (unsigned long long)evict_draw(P.seed, gid, t, pass, j) < P.beta_thresh;
+                                if (ev) keep &= ~(1u << (j & 31));
                             }
-                            left += __popc(__ballot_sync(KV_FULL, act && !ev));
-                            uint32_t evm = __ballot_sync(KV_FULL, ev);
-                            if (evm) {
-                                evictions += __popc(evm);
-                                sumc -= warp_sum_i64(ev ? (long long)(pj + oj) : 0ll);
-                                const int mn = warp_min_i32(ev ? j : KV_INF);
-                                if (mn < h) { h = mn; hstale = true; }
-                                if (ev) {
-                                    q_insert(Q, j);
-                                    if (P.completion) P.completion[off + j] = -1;
-                                    if (P.start) P.start[off + j] = -1;
-                                }
-                                if (POL == POL_ALPHA_BETA) {
-                                    while (evm) {                       // remove its ramp
-                                        const int l = __ffs(evm) - 1;
-                                        evm &= evm - 1;
-                                        const int s_ = __shfl_sync(KV_FULL, sj, l);
-                                        const int p_ = __shfl_sync(KV_FULL, pj, l);
-                                        const int o_ = __shfl_sync(KV_FULL, oj, l);
-                                        __syncwarp();
-                                        ring_ramp(S.prof, mask, t, p_ + o_ - t, s_ + t - p_, -1);
-                                    }
+                        }
+                        left += __popc(__ballot_sync(KV_FULL, act && !ev));
+                        uint32_t evm = __ballot_sync(KV_FULL, ev);
+                        if (evm) {
+                            evictions += __popc(evm);
+                            sumc -= warp_sum_i64(ev ? (long long)(pj + oj) : 0ll);
+                            const int mn = warp_min_i32(ev ? j : KV_INF);
+                            if (mn < h) { h = mn; hstale = true; }
+                            if (ev) {
+                                q_insert(Q, j);
+                                if (P.completion) P.completion[off + j] = -1;
+                                if (P.start) P.start[off + j] = -1;
+                            }
+                            if (POL == POL_ALPHA_BETA) {
+                                while (evm) {                       // remove its ramp
+                                    const int l = __ffs(evm) - 1;
+                                    evm &= evm - 1;
+                                    const int s_ = __shfl_sync(KV_FULL, sj, l);
+                                    const int p_ = __shfl_sync(KV_FULL, pj, l);
+                                    const int o_ = __shfl_sync(KV_FULL, oj, l);
+                                    __syncwarp();
+                                    ring_ramp(S.prof, mask, t, p_ + o_ - t, s_ + t - p_, -1);
                                 }
                             }
                         }
-                        if (wi < nw) S.infl[wi] = keep;
                     }
-                    __syncwarp();
-                    if (POL == POL_ALPHA) {
-                        for (int i = lane; i < L; i += 32) S.prof[i] = 0;
-                        __syncwarp();
-                        mem = 0;
-                        break;
-                    }
-                    left = __shfl_sync(KV_FULL, left, 0);
-                    mem = S.prof[(t + 1) & mask];
-                    if (mem <= M || left == 0) break;
+                    if (wi < nw) S.infl[wi] = keep;
                 }
+                __syncwarp();
+                if (POL == POL_ALPHA) {
+                    for (int i = lane; i < L; i += 32) S.prof[i] = 0;
+                    __syncwarp();
+                    mem = 0;
+                    cycle = next_at_clear == next && evictions - ev_before == adm_since_clear;
+                    next_at_clear = next;
+                    adm_since_clear = 0;
+                    break;
+                }
+                mem = S.prof[(t + 1) & mask];
+                if (mem <= M || left == 0) break;
             }
-            if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
-            if (had_R || !idle_before) ++rounds;
         }
+        if (cycle) { status = ST_LIVELOCK; break; }
+        if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
+        if (had_R || !idle_before) ++rounds;
         __syncwarp();
         const int mnow = S.prof[(t + 1) & mask];                   // Mem(t+1) of the batch
         peak = max(peak, mnow);
@@ -311,6 +369,32 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
         if (lane == 0) S.prof[(t + 1) & mask] = 0;
         __syncwarp();
         ++t;
+
+        // Rounds r = t, t+1, ... in which nothing can happen: no overflow (Mem(r+1) <= M),
+        // S non-empty, and either the FCFS head stays over the threshold (a newcomer never
+        // precedes it) or, with R empty, nothing arrives.  Found 32 at a time by a ballot
+        // over the ring; their counters are accumulated without iterating them.
+        if (multi && mem_prev > 0) {
+            const int sh = h != KV_INF ? (hstale ? (int)fetch(h).x : (int)he.x) : 0;
+            for (;;) {
+                const int r = t + lane;
+                const int v = S.prof[(r + 1) & mask];
+                const bool quiet = r <= cap && v > 0 && v <= M &&
+                                   (h != KV_INF ? (long long)v + sh + 1 > B : r < a_next);
+                const uint32_t qm = __ballot_sync(KV_FULL, quiet);
+                const int k = qm == KV_FULL ? 32 : __ffs(~qm) - 1;   // quiet rounds t..t+k-1
+                if (k == 0) break;
+                peak = max(peak, warp_max_i32(lane < k ? v : 0));
+                mem_prev = __shfl_sync(KV_FULL, v, k - 1);
+                __syncwarp();
+                if (lane < k) S.prof[(r + 1) & mask] = 0;
+                __syncwarp();
+                rounds += k;
+                if (h != KV_INF) drounds += k;
+                t += k;
+                if (k < 32) break;
+            }
+        }
     }
 
     if (status != ST_OK) {

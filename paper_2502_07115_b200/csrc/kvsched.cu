@@ -329,6 +329,7 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     P.policy = pol->policy;
     P.alpha_num = pol->alpha_num;
     P.alpha_den = pol->alpha_den > 0 ? pol->alpha_den : 1;
+    P.flags = pol->flags;
     P.beta_thresh = pol->beta_thresh;
     P.seed = pol->seed;
     P.round_cap = pol->round_cap;
@@ -370,9 +371,10 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
 #undef KV_SMALL
     }
 
-    // ring kernel: profile ring L > max_len (and > M - 1 for the projection window)
+    // ring kernel: profile ring L > max_len + 32 (a candidate's window plus the 32-round
+    // look-ahead of ring_first_fit)
     P.NP = next_pow2(max_req < 32 ? 32 : max_req);
-    P.L = next_pow2(max_len + 1);
+    P.L = next_pow2(max_len + 33);
     P.warp_bytes = ring_warp_bytes(P.L, P.NP, pol->policy);
     const int smem = P.warp_bytes;
     if ((size_t)smem > c->max_smem_optin)

@@ -16,13 +16,13 @@ struct KParams {
     const int *mem;
     unsigned long long id0;
     // policy
-    int policy, alpha_num, alpha_den;
+    int policy, alpha_num, alpha_den, flags;
     unsigned long long beta_thresh, seed;
     long long round_cap;
     // capacity (validated hints)
     int max_requests, max_mem, max_len;
     int NP;                     // per-warp rank capacity (pow2 >= max_requests, >= 32)
-    int L;                      // ring kernel: profile ring length (pow2 > max_len)
+    int L;                      // ring kernel: profile ring length (pow2 > max_len + 32)
     int warp_bytes;             // dynamic shared memory per warp
     // outputs (any may be null)
     int *completion, *start;

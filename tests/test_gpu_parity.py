@@ -145,15 +145,16 @@ def test_am1_paper_draw(K, ctx, oracle_mod):
     check(K, ctx, oracle_mod, b, 0, "AM1-paper")
 
 
+@pytest.mark.parametrize("flags", [0, 1])
 @pytest.mark.parametrize("pol", [0, 1, 2, 3])
 @pytest.mark.parametrize("mhi", [64, 300])
-def test_fuzz_ragged(K, ctx, oracle_mod, pol, mhi):
+def test_fuzz_ragged(K, ctx, oracle_mod, pol, mhi, flags):
     """Ragged batches (empty instances included), M up to 64 (fused kernel for MC) and up to
-    300 (ring kernel)."""
+    300 (ring kernel), both evaluation modes."""
     b = W.random_small(3000, 15 + mhi, n_max=70, M_lo=4, M_hi=mhi, a_max=60)
     assert (b.sizes() == 0).any()
     kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=77) if pol >= 2 else {}
-    check(K, ctx, oracle_mod, b, pol, f"fuzz M<={mhi}", **kw)
+    check(K, ctx, oracle_mod, b, pol, f"fuzz M<={mhi}", flags=flags, **kw)
 
 
 @pytest.mark.parametrize("pol", [0, 1])
@@ -161,9 +162,10 @@ def test_ring_kernel_on_small_budgets(K, ctx, oracle_mod, pol):
     """Force the shared-memory ring kernel (hint max_mem > 64) on small-M instances: both
     kernels must reproduce the oracle."""
     b = W.random_small(3000, 16, n_max=70, M_lo=4, M_hi=64, a_max=60)
-    check(K, ctx, oracle_mod, b, pol, "ring on small M", hints=(70, 65, 64))
     c = W.am2(2000, 17)
-    check(K, ctx, oracle_mod, c, pol, "ring on C5", hints=(c.max_requests(), 65, 64))
+    for flags in (0, 1):
+        check(K, ctx, oracle_mod, b, pol, "ring on small M", hints=(70, 65, 64), flags=flags)
+        check(K, ctx, oracle_mod, c, pol, "ring on C5", hints=(c.max_requests(), 65, 64), flags=flags)
 
 
 def test_prediction_overestimate_small(K, ctx, oracle_mod):
@@ -178,7 +180,8 @@ def test_c4_policies(K, ctx, oracle_mod, name, pol, alpha, beta):
     b = W.c4(48, 19)
     polid = {"mcsf": 0, "mcbench": 1, "alpha": 2, "alpha_beta": 3}[pol]
     kw = dict(alpha=alpha or (0, 1), beta_thresh=W.beta_threshold(beta or 0.0), seed=2025)
-    check(K, ctx, oracle_mod, b, polid, name, **kw)
+    for flags in (0, 1):
+        check(K, ctx, oracle_mod, b, polid, name, flags=flags, **kw)
 
 
 @pytest.mark.parametrize("pol", [2, 3])
@@ -186,8 +189,9 @@ def test_alpha_with_evictions(K, ctx, oracle_mod, pol):
     """Tight budgets force overflows, evictions and (for alpha-greedy) livelocks."""
     b = W.random_small(3000, 20, n_max=40, M_lo=10, M_hi=80, a_max=20)
     for alpha in ((1, 10), (0, 1), (3, 10)):
-        o, g = check(K, ctx, oracle_mod, b, pol, f"alpha={alpha}", alpha=alpha,
-                     beta_thresh=W.beta_threshold(0.25), seed=5)
+        for flags in (0, 1):
+            o, g = check(K, ctx, oracle_mod, b, pol, f"alpha={alpha}", alpha=alpha,
+                         beta_thresh=W.beta_threshold(0.25), seed=5, flags=flags)
     assert o["evictions"].sum() > 0
     assert (o["status"] == 2).any() or pol == 3
 
@@ -196,7 +200,8 @@ def test_alpha_with_evictions(K, ctx, oracle_mod, pol):
 @pytest.mark.parametrize("pol", [0, 1])
 def test_c3_trace(K, ctx, oracle_mod, lam, pol):
     b = W.c3(2, 21, lam)
-    check(K, ctx, oracle_mod, b, pol, f"C3 lam={lam}")
+    for flags in (0, 1):
+        check(K, ctx, oracle_mod, b, pol, f"C3 lam={lam}", flags=flags)
 
 
 @pytest.mark.parametrize("pol", [0, 1, 2, 3])
@@ -204,8 +209,8 @@ def test_round_cap_livelock(K, ctx, oracle_mod, pol):
     """An explicit round cap stops runs mid-flight: both sides report LIVELOCK with the same
     partial counters and completions."""
     b = W.random_small(2000, 22, n_max=40, M_lo=6, M_hi=120, a_max=30)
-    for cap in (5, 17, 40):
-        kw = dict(round_cap=cap)
+    for cap, flags in ((5, 0), (17, 1), (40, 0), (40, 1), (61, 0)):
+        kw = dict(round_cap=cap, flags=flags)
         if pol >= 2:
             kw.update(alpha=(1, 10), beta_thresh=W.beta_threshold(0.4), seed=3)
         o, _ = check(K, ctx, oracle_mod, b, pol, f"cap={cap}", **kw)
