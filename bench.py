@@ -232,24 +232,15 @@ def main():
     pol = policy_of(K, args.policy)
     id0 = rank * batch.n_inst
     if world > 1:
-        gathered = torch.empty((world, 3, batch.n_inst), dtype=torch.int64, device=dev)
-        mine = torch.empty((3, batch.n_inst), dtype=torch.int64, device=dev)
-        totals = torch.empty(4, dtype=torch.int64, device=dev)
+        from paper_2502_07115_b200 import dist as D
 
     def step():
         ctx.run(off, req, mem, pol, out, id0=id0, hints=hints)
         if world > 1:
-            # the north star's only collective: gather per-instance (TEL, rounds, status) and
-            # reduce the totals over NVLink (NCCL)
-            mine[0].copy_(out["tel"][:batch.n_inst])
-            mine[1].copy_(out["rounds"][:batch.n_inst])
-            mine[2].copy_(out["status"][:batch.n_inst])
-            dist.all_gather_into_tensor(gathered, mine)
-            totals[0] = out["tel"][:batch.n_inst].clamp(min=0).sum()
-            totals[1] = out["rounds"][:batch.n_inst].clamp(min=0).sum()
-            totals[2] = (out["status"][:batch.n_inst] == 0).sum()
-            totals[3] = batch.n_inst
-            dist.all_reduce(totals)
+            # the north star's only collective: gather per-instance (TEL, rounds, status) of
+            # every shard and reduce the totals (NCCL over NVLink / NVSwitch)
+            D.gather_results(D.pack_results(out, batch.n_inst, batch.n_inst, dev))
+            D.reduce_totals(out, batch.n_inst)
 
     for _ in range(max(args.warmup, 0)):
         step()

@@ -1,0 +1,83 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the sharding and result exchange.
+
+Each rank takes its shard of a batch, computes that shard's per-instance results (here with
+the CPU oracle: the host-side exchange logic is what is under test), and the gathered /
+reduced results must equal the whole-batch run.  The alpha-beta RNG is keyed by the global
+instance id, so the shard results themselves must not depend on the split either.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import workloads as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2502_07115_b200 import dist as D
+        b = W.random_small(301, 7, n_max=30, M_lo=10, M_hi=60, a_max=20)
+        sizes = [D.shard_bounds(b.n_inst, world, r, weights=b.sizes())[1] -
+                 D.shard_bounds(b.n_inst, world, r, weights=b.sizes())[0] for r in range(world)]
+        lo, hi = D.shard_bounds(b.n_inst, world, rank, weights=b.sizes())
+        sub = b.subset(range(lo, hi))
+        o = oracle.simulate_batch(sub.offset, sub.req, sub.mem, oracle.ALPHA_BETA, alpha=(1, 10),
+                                  beta_thresh=W.beta_threshold(0.3), seed=11, gid0=lo, nthreads=1)
+        out = {k: torch.from_numpy(np.asarray(o[k], dtype=np.int64)) for k in ("tel", "rounds", "status")}
+        local = D.pack_results(out, hi - lo, max(sizes), "cpu")
+        g = D.gather_results(local)
+        tot = D.reduce_totals(out, hi - lo)
+        if rank == 0:
+            q.put((D.unpad(g, sizes).numpy(), tot.numpy(), sizes))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_bounds():
+    from paper_2502_07115_b200 import dist as D
+    for n, w in ((10, 3), (0, 2), (7, 8), (1000, 8)):
+        cuts = [D.shard_bounds(n, w, r) for r in range(w)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == n
+        assert all(cuts[r][1] == cuts[r + 1][0] for r in range(w - 1))
+        assert max(b - a for a, b in cuts) - min(b - a for a, b in cuts) <= 1
+    wts = np.array([1] * 90 + [100] * 10)
+    cuts = [D.shard_bounds(100, 2, r, weights=wts) for r in range(2)]
+    assert cuts[0][1] < 95 and cuts[0][0] == 0 and cuts[1][1] == 100
+
+
+def test_gloo_world2_gather_equals_whole_batch():
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    rows, tot, sizes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    b = W.random_small(301, 7, n_max=30, M_lo=10, M_hi=60, a_max=20)
+    whole = oracle.simulate_batch(b.offset, b.req, b.mem, oracle.ALPHA_BETA, alpha=(1, 10),
+                                  beta_thresh=W.beta_threshold(0.3), seed=11, gid0=0)
+    assert sum(sizes) == b.n_inst and min(sizes) > 0
+    assert np.array_equal(rows[0], whole["tel"])
+    assert np.array_equal(rows[1], whole["rounds"])
+    assert np.array_equal(rows[2], whole["status"])
+    ok = whole["status"] == 0
+    assert tot.tolist() == [int(whole["tel"][ok].sum()), int(whole["rounds"][ok].sum()), int(ok.sum()), b.n_inst]
