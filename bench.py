@@ -280,7 +280,7 @@ def main():
 
     # roofline of the simulation kernel: algorithmic bytes per launch / mean launch time
     kname = ctx.last_kernel()
-    k_ms = st["sim_kernel_ms"] / max(st["sim_kernel_launches"], 1)
+    k_ms = st["sim_kernel_ms"] / max(args.steps, 1)          # simulation kernel time per step
     alg = algorithmic_bytes(batch, fields)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak_gbs = peaks.get("hbm_gbs", 6650.0)
@@ -288,7 +288,8 @@ def main():
     traffic = ncu_traffic(kname)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
             "frac": achieved / peak_gbs, "traffic": traffic, "alg_bytes_per_launch": alg,
-            "kernel_ms": k_ms, "peak_source": "measured" if peaks else "fallback",
+            "kernel_ms": k_ms, "sim_launches_per_step": st["sim_kernel_launches"] / max(args.steps, 1),
+            "peak_source": "measured" if peaks else "fallback",
             "kernel_share_of_step": (st["sim_kernel_ms"] / args.steps) / (ms_max / args.steps) if args.steps else None}
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region

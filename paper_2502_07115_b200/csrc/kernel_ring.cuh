@@ -1,10 +1,15 @@
 // kernel_ring.cuh -- per-instance warp simulator for any budget M (all four policies).
 //
-// Same round structure as kernel_small.cuh, but the memory profile is a ring of L int32
-// slots in shared memory (slot r & (L-1) holds absolute round r, L a power of two larger
-// than every request length + 32), so a candidate's Eq. 5 test and its admission
-// are ceil(w/32) warp-wide passes over its own window.  Per-request data stay in HBM/L2
-// and are fetched when a request reaches the head of the queue.
+// Same round structure as kernel_small.cuh, but the memory profile lives in a ring of L
+// int32 slots in shared memory holding the exact profile of the window [t+1, t+L] (slot
+// r & (L-1) = absolute round r), so a candidate's Eq. 5 test and its admission are
+// ceil(w/32) warp-wide passes over its own window.  L is at most KV_RING_SHORT (2048) so
+// that ~20 warps fit an SM; the rare requests whose ramp reaches past the window ("long",
+// w > L) are kept one per lane in a LongList: slots entering the window are initialised from
+// it and positions beyond the window are computed from it.  An instance that ever has more
+// than 32 long requests in flight is handed to a second launch with a ring covering every
+// request (status RETRY, internal).  Per-request data stay in HBM/L2 and are fetched when a
+// request reaches the head of the queue.
 //
 //   MC-SF / MC-Benchmark : ring = projected memory of S (Eq. 5 LHS), as in the small kernel.
 //                           A blocked head is resolved over the next 32 rounds per pass
@@ -43,32 +48,109 @@ __device__ __forceinline__ void ring_ramp(int *prof, int mask, int t, int e, int
     for (int tau = lane_id() + 1; tau <= e; tau += 32) prof[(t + tau) & mask] += sign * (base + tau);
 }
 
-// max of Prof(t+tau) over tau in [1, d] and zero tau in [1, z]
-__device__ __forceinline__ int ring_max_zero(int *prof, int mask, int t, int d, int z)
+// In-flight requests whose ramp reaches past the ring window: one per lane.  Active at
+// absolute rounds (p, e], holding s + r - p at round r (Eq. 3).  `used` is warp-uniform.
+struct LongList {
+    int p, s, e, idx;
+    uint32_t used;
+};
+
+// sum over long requests active at absolute round r of (s + r - p); r may differ per lane,
+// all lanes must call
+__device__ __forceinline__ int long_prof(const LongList &G, int r)
 {
     int v = 0;
-    const int e = max(d, z);
-    for (int tau = lane_id() + 1; tau <= e; tau += 32) {
-        int *q = &prof[(t + tau) & mask];
-        if (tau <= d) v = max(v, *q);
-        if (tau <= z) *q = 0;
+    uint32_t m = G.used;
+    while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const int p = __shfl_sync(KV_FULL, G.p, l), s = __shfl_sync(KV_FULL, G.s, l);
+        const int e = __shfl_sync(KV_FULL, G.e, l);
+        if (p < r && r <= e) v += s + r - p;
     }
+    return v;
+}
+
+__device__ __forceinline__ bool long_add(LongList &G, int p, int s, int e, int idx)
+{
+    if (G.used == KV_FULL) return false;
+    const int l = __ffs(~G.used) - 1;
+    if (lane_id() == l) { G.p = p; G.s = s; G.e = e; G.idx = idx; }
+    G.used |= 1u << l;
+    return true;
+}
+
+__device__ __forceinline__ void long_remove_idx(LongList &G, int idx)
+{
+    G.used &= ~__ballot_sync(KV_FULL, ((G.used >> lane_id()) & 1u) && G.idx == idx);
+}
+
+// Profile at window position u (absolute round t+u): ring inside the window, long list beyond.
+__device__ __forceinline__ int prof_at(const int *prof, int mask, int L, const LongList &G, int t, int u)
+{
+    const int far = G.used ? long_prof(G, t + u) : 0;
+    return u <= L ? prof[(t + u) & mask] : far;
+}
+
+// Advance the window start from t to tn (> t) and return max Prof(r) over r in [t+1, E]
+// (E <= tn; the occupancy of the batches of rounds t..E-1).  Slots leaving the window are
+// re-initialised for the rounds entering it, from the long list.
+__device__ __forceinline__ int ring_jump(int *prof, int mask, int L, LongList &G, int t, int E, int tn)
+{
+    const int lane = lane_id();
+    int v = 0;
+    const int dn = max(min(E - t, L), 0);
+    for (int base = 1; base <= dn; base += 32) {
+        const int tau = base + lane;
+        if (tau <= dn) v = max(v, prof[(t + tau) & mask]);
+    }
+    if (G.used && E - t > L) {
+        // rounds beyond the old window: only long requests; maximum at an end point or at E
+        const bool own = ((G.used >> lane) & 1u) && G.e > t + L && G.e <= E;
+        v = max(v, long_prof(G, own ? G.e : E));
+    }
+    __syncwarp();
+    if (tn - t <= L) {
+        for (int base = 1; base <= tn - t; base += 32) {
+            const int tau = base + lane;
+            const int far = G.used ? long_prof(G, t + tau + L) : 0;
+            if (tau <= tn - t) prof[(t + tau) & mask] = far;
+        }
+    } else {
+        for (int j0 = 0; j0 < L; j0 += 32) {                     // whole window rewritten
+            const int j = j0 + lane;
+            const int r = tn + 1 + ((j - (tn + 1)) & mask);       // round of slot j in [tn+1, tn+L]
+            const int far = G.used ? long_prof(G, r) : 0;
+            prof[j] = far;
+        }
+    }
+    G.used &= ~__ballot_sync(KV_FULL, ((G.used >> lane) & 1u) && G.e <= tn + L);   // now inside
     __syncwarp();
     return warp_max_i32(v);
 }
 
-// First offset D in [0, 31] at which the head (s, w) satisfies Eq. 5 while the ring only
-// advances; 32 if it is blocked at all of them.  Ring position u = D + tau rules out the
-// offsets D in [u-w, u-1] with Prof(u) + s + u - D > M (see first_fit_offset in
-// kernel_small.cuh); positions beyond w + 31 cannot reach D <= 31.
-__device__ __forceinline__ int ring_first_fit(const int *prof, int mask, int t, int s, int w, int M)
+// Admit a ramp s + tau, tau in [1, w], started at t: the window part into the ring, the
+// rest via the long list.  false = long list full.
+__device__ __forceinline__ bool ring_admit(int *prof, int mask, int L, LongList &G, int t, int w, int s, int idx)
+{
+    ring_ramp(prof, mask, t, min(w, L), s, +1);
+    if (w > L) return long_add(G, t, s, t + w, idx);
+    return true;
+}
+
+// First offset D in [0, 31] at which the head (s, w) satisfies Eq. 5 while the profile only
+// advances; 32 if it is blocked at all of them.  Position u = D + tau rules out the offsets
+// D in [u-w, u-1] with Prof(u) + s + u - D > M (see first_fit_offset in kernel_small.cuh);
+// positions beyond w + 31 cannot reach D <= 31.
+__device__ __forceinline__ int ring_first_fit(const int *prof, int mask, int L, const LongList &G, int t,
+                                              int s, int w, int M)
 {
     const int lane = lane_id();
     const int room = M - s;
     unsigned cov = 0u;
     for (int base = 1; base <= w + 31; base += 32) {
         const int u = base + lane;
-        const int D = prof[(t + u) & mask];
+        const int D = prof_at(prof, mask, L, G, t, u);
         const int lo = max(u - w, 0);
         const int hi = min(min(u - 1, D + u - room - 1), 31);
         if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
@@ -150,6 +232,9 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     // arrival pointer then; a clear-all that evicts everything admitted since the previous
     // one (nothing completed) with no arrival in between repeats that cycle for ever.
     int adm_since_clear = 0, next_at_clear = -1;
+    LongList G;
+    G.p = G.s = G.e = G.idx = 0;
+    G.used = 0u;
 
     auto fetch = [&](int r) -> uint4 {
         if (POL == POL_MCSF) return P.rq[off + r];
@@ -162,7 +247,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
             if (MC) {
                 if (a_next == KV_INF) {                        // drain
                     const int E = min(maxc, cap + 1);
-                    if (E > t) peak = max(peak, ring_max_zero(S.prof, mask, t, min(E - t, L), 0));
+                    if (E > t) peak = max(peak, ring_jump(S.prof, mask, L, G, t, E, t));
                     if (maxc > t) rounds += maxc - t;
                     if (maxc >= cap + 1) status = ST_LIVELOCK;
                     break;
@@ -170,8 +255,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 const int tn = a_next;
                 if (tn > t) {                                  // skip rounds t..tn-1
                     const int E = min(tn, cap + 1);
-                    const int d = E > t ? min(E - t, L) : 0;
-                    peak = max(peak, ring_max_zero(S.prof, mask, t, d, min(tn - t, L)));
+                    peak = max(peak, ring_jump(S.prof, mask, L, G, t, E, tn));
                     rounds += max(0, min(tn, maxc) - t);
                     if (tn > cap) { status = ST_LIVELOCK; break; }
                     t = tn;
@@ -212,17 +296,20 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 if (!head_fits) {
                     int d;
                     if (multi) {
-                        d = ring_first_fit(S.prof, mask, t, s, w, M);
+                        d = ring_first_fit(S.prof, mask, L, G, t, s, w, M);
                     } else {
                         bool bad_ = false;
-                        for (int tau = lane + 1; tau <= w; tau += 32)
-                            bad_ |= S.prof[(t + tau) & mask] + s + tau > M;
+                        for (int base = 1; base <= w; base += 32) {
+                            const int tau = base + lane;
+                            const int v = prof_at(S.prof, mask, L, G, t, tau);
+                            bad_ |= tau <= w && v + s + tau > M;
+                        }
                         d = __any_sync(KV_FULL, bad_) ? 1 : 0;
                     }
                     if (d > 0) { jump = d; blocked_through = d == 32; break; }   // Eq. 5 violated
                 }
                 head_fits = false;
-                ring_ramp(S.prof, mask, t, w, s, +1);
+                if (!ring_admit(S.prof, mask, L, G, t, w, s, idx)) { status = ST_RETRY; break; }
                 const int c = t + o;
                 if (lane == 0) {
                     if (P.completion) P.completion[off + idx] = c;
@@ -235,6 +322,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 if (h == KV_INF) break;
                 he = fetch(h);
             }
+            if (status == ST_RETRY) break;
             if (jump > 1) {
                 int T = t + min(jump, cap + 1 - t);
                 if (POL == POL_MCSF) {
@@ -253,7 +341,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
             }
             drounds += jump;
             rounds += jump;
-            peak = max(peak, ring_max_zero(S.prof, mask, t, jump, jump));
+            peak = max(peak, ring_jump(S.prof, mask, L, G, t, t + jump, t + jump));
             t += jump;
             continue;
         }
@@ -270,7 +358,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 const int s = (int)he.x, o = (int)he.z, idx = (int)he.w;
                 if (Lnext + s + 1 > B) break;                   // (1-alpha)M threshold
                 Lnext += s + 1;
-                ring_ramp(S.prof, mask, t, o, s, +1);
+                if (!ring_admit(S.prof, mask, L, G, t, o, s, idx)) { status = ST_RETRY; break; }
                 const int c = t + o;
                 if (lane == 0) {
                     if (P.completion) P.completion[off + idx] = c;
@@ -287,6 +375,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 he = fetch(h);
             }
         }
+        if (status == ST_RETRY) break;
         __syncwarp();
         int mem = S.prof[(t + 1) & mask];
         bool cycle = false;
@@ -336,8 +425,10 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                                     const int s_ = __shfl_sync(KV_FULL, sj, l);
                                     const int p_ = __shfl_sync(KV_FULL, pj, l);
                                     const int o_ = __shfl_sync(KV_FULL, oj, l);
+                                    const int j_ = __shfl_sync(KV_FULL, j, l);
                                     __syncwarp();
-                                    ring_ramp(S.prof, mask, t, p_ + o_ - t, s_ + t - p_, -1);
+                                    ring_ramp(S.prof, mask, t, min(p_ + o_ - t, L), s_ + t - p_, -1);
+                                    long_remove_idx(G, j_);
                                 }
                             }
                         }
@@ -348,6 +439,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 if (POL == POL_ALPHA) {
                     for (int i = lane; i < L; i += 32) S.prof[i] = 0;
                     __syncwarp();
+                    G.used = 0u;
                     mem = 0;
                     cycle = next_at_clear == next && evictions - ev_before == adm_since_clear;
                     next_at_clear = next;
@@ -362,12 +454,9 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
         if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
         if (had_R || !idle_before) ++rounds;
         __syncwarp();
-        const int mnow = S.prof[(t + 1) & mask];                   // Mem(t+1) of the batch
+        const int mnow = ring_jump(S.prof, mask, L, G, t, t + 1, t + 1);   // Mem(t+1) of the batch
         peak = max(peak, mnow);
         mem_prev = mnow;
-        __syncwarp();
-        if (lane == 0) S.prof[(t + 1) & mask] = 0;
-        __syncwarp();
         ++t;
 
         // Rounds r = t, t+1, ... in which nothing can happen: no overflow (Mem(r+1) <= M),
@@ -384,11 +473,8 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 const uint32_t qm = __ballot_sync(KV_FULL, quiet);
                 const int k = qm == KV_FULL ? 32 : __ffs(~qm) - 1;   // quiet rounds t..t+k-1
                 if (k == 0) break;
-                peak = max(peak, warp_max_i32(lane < k ? v : 0));
                 mem_prev = __shfl_sync(KV_FULL, v, k - 1);
-                __syncwarp();
-                if (lane < k) S.prof[(r + 1) & mask] = 0;
-                __syncwarp();
+                peak = max(peak, ring_jump(S.prof, mask, L, G, t, t + k, t + k));
                 rounds += k;
                 if (h != KV_INF) drounds += k;
                 t += k;
@@ -397,6 +483,10 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
         }
     }
 
+    if (status == ST_RETRY) {               // rerun by the full-ring launch (kvsched.cu)
+        if (lane == 0) P.retry_list[atomicAdd(P.retry_count, 1ull)] = inst;
+        return;
+    }
     if (status != ST_OK) {
         for (int k = next + lane; k < n; k += 32) {
             if (P.completion) P.completion[off + k] = -1;
@@ -442,14 +532,16 @@ __global__ void __launch_bounds__(128) k_ring(const KParams P)
     S.sm = reinterpret_cast<uint32_t *>(base + P.L * 4 + (P.NP / 32) * 4);
     S.infl = reinterpret_cast<uint32_t *>(base + P.L * 4 + (P.NP / 32) * 4 + 128);
 
-    long long inst = 0;
-    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
-    inst = __shfl_sync(KV_FULL, inst, 0);
-    while (inst < P.n_inst) {
+    // work item w is instance w, or work_list[w] for the full-ring rerun of RETRY instances
+    const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+    long long w = 0;
+    if (lane == 0) w = atomicAdd(P.counter, 1ull);
+    w = __shfl_sync(KV_FULL, w, 0);
+    while (w < n_work) {
         long long nxt = 0;
         if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
-        ring_instance<POL>(P, inst, S);
-        inst = __shfl_sync(KV_FULL, nxt, 0);
+        ring_instance<POL>(P, P.work_list ? P.work_list[w] : w, S);
+        w = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();
     }
 }

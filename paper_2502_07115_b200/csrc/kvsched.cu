@@ -21,6 +21,9 @@ namespace {
 constexpr int kBlock = 128;                   // 4 warps, one instance per warp
 constexpr int kSmallMaxMem = 64;              // register profile covers tau = 1..64
 constexpr int kSmallMaxRequests = 16384;      // 14-bit idx in the packed word
+#ifndef KV_RING_SHORT
+#define KV_RING_SHORT 2048                    // ring window of the first k_ring launch
+#endif
 
 struct DevBuf {
     void *p = nullptr;
@@ -36,7 +39,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, total;
+    DevBuf counter, bounds, rq, arank, pstart, total, retry;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -371,15 +374,23 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
 #undef KV_SMALL
     }
 
-    // ring kernel: profile ring L > max_len + 32 (a candidate's window plus the 32-round
-    // look-ahead of ring_first_fit)
+    // ring kernel.  The first launch uses a window of L_short <= KV_RING_SHORT slots (long
+    // requests go through the per-lane long list); instances that overflow the list are
+    // rerun by a second launch whose ring covers every request plus the 32-round look-ahead.
     P.NP = next_pow2(max_req < 32 ? 32 : max_req);
-    P.L = next_pow2(max_len + 33);
+    const int L_full = next_pow2(max_len + 33);
+    const int L_short = L_full < KV_RING_SHORT ? L_full : KV_RING_SHORT;
+    P.L = L_short;
     P.warp_bytes = ring_warp_bytes(P.L, P.NP, pol->policy);
-    const int smem = P.warp_bytes;
-    if ((size_t)smem > c->max_smem_optin)
-        return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)", smem, P.L, P.NP);
+    if ((size_t)ring_warp_bytes(L_full, P.NP, pol->policy) > c->max_smem_optin)
+        return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
+                    ring_warp_bytes(L_full, P.NP, pol->policy), L_full, P.NP);
+    if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
+    P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
+    P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
+    CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
     const size_t slots = (size_t)inst->n_instances * (size_t)max_req;
+    const char *name = "";
     if (pol->policy == SCHED_MCSF) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
         // offsets are relative to the batch: scratch slot = request row (n_req <= slots)
@@ -392,13 +403,31 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
                                                              reinterpret_cast<int *>(c->arank.p));
         CUDA_TRY(c, cudaGetLastError());
         c->launches++;
-        return launch_sim(c, k_ring<POL_MCSF>, P, smem, "k_ring<MCSF>");
+    } else if (pol->policy >= SCHED_ALPHA) {
+        if ((rc = grow(c, c->pstart, slots * 4))) return rc;
+        P.pstart = reinterpret_cast<int *>(c->pstart.p);
     }
-    if (pol->policy == SCHED_MC_BENCH) return launch_sim(c, k_ring<POL_MCBENCH>, P, smem, "k_ring<MCBENCH>");
-    if ((rc = grow(c, c->pstart, slots * 4))) return rc;
-    P.pstart = reinterpret_cast<int *>(c->pstart.p);
-    if (pol->policy == SCHED_ALPHA) return launch_sim(c, k_ring<POL_ALPHA>, P, smem, "k_ring<ALPHA>");
-    return launch_sim(c, k_ring<POL_ALPHA_BETA>, P, smem, "k_ring<ALPHA_BETA>");
+    auto launch_ring = [&](const KParams &Q) -> int {
+        switch (pol->policy) {
+        case SCHED_MCSF: name = "k_ring<MCSF>"; return launch_sim(c, k_ring<POL_MCSF>, Q, Q.warp_bytes, name);
+        case SCHED_MC_BENCH: name = "k_ring<MCBENCH>"; return launch_sim(c, k_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);
+        case SCHED_ALPHA: name = "k_ring<ALPHA>"; return launch_sim(c, k_ring<POL_ALPHA>, Q, Q.warp_bytes, name);
+        default: name = "k_ring<ALPHA_BETA>"; return launch_sim(c, k_ring<POL_ALPHA_BETA>, Q, Q.warp_bytes, name);
+        }
+    };
+    if ((rc = launch_ring(P))) return rc;
+    if (L_short < L_full) {
+        KParams Q = P;
+        Q.L = L_full;
+        Q.warp_bytes = ring_warp_bytes(L_full, P.NP, pol->policy);
+        Q.work_list = P.retry_list;
+        Q.work_count = P.retry_count;
+        Q.retry_list = nullptr;          // the full ring never overflows (no long requests)
+        Q.retry_count = nullptr;
+        CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+        if ((rc = launch_ring(Q))) return rc;
+    }
+    return SCHED_OK;
 }
 
 int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
@@ -533,7 +562,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->total, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->total, &c->retry, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {

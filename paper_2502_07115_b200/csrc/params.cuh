@@ -6,7 +6,7 @@
 namespace kv {
 
 enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3 };
-enum { ST_OK = 0, ST_INVALID = 1, ST_LIVELOCK = 2, ST_UNSUPPORTED = 3 };
+enum { ST_OK = 0, ST_INVALID = 1, ST_LIVELOCK = 2, ST_UNSUPPORTED = 3, ST_RETRY = 4 /* internal */ };
 
 struct KParams {
     // batch
@@ -33,6 +33,10 @@ struct KParams {
     int *pstart;                // alpha policies: start round of each request (scratch)
     const uint4 *rq;            // MC-SF ring path: per-rank entries {s, o~, o, idx}
     const int *arank;           // MC-SF ring path: rank of request idx
+    long long *retry_list;      // ring kernel: instances handed to the full-ring launch
+    unsigned long long *retry_count;
+    const long long *work_list; // full-ring launch: the instances to (re)run
+    const unsigned long long *work_count;
 };
 
 // Lane 0 writes the per-instance outputs.

@@ -184,6 +184,34 @@ def test_c4_policies(K, ctx, oracle_mod, name, pol, alpha, beta):
         check(K, ctx, oracle_mod, b, polid, name, flags=flags, **kw)
 
 
+def _long_batch(n_inst, seed, n_max=60, M_lo=3000, M_hi=9000, o_max=6000, a_max=400):
+    """Instances whose requests often outlast the 2048-round ring window of k_ring."""
+    g = np.random.default_rng(seed)
+    insts = []
+    for _ in range(n_inst):
+        M = int(g.integers(M_lo, M_hi + 1))
+        n = int(g.integers(0, n_max + 1))
+        a = np.sort(g.integers(0, a_max + 1, n))
+        s_ = g.integers(1, 60, n)
+        o = np.minimum(g.integers(1, o_max + 1, n), M - s_)
+        insts.append((np.stack([a, s_, o, o], 1).astype(np.int32), M))
+    return W.from_instances(insts)
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+@pytest.mark.parametrize("pol", [0, 1, 2, 3])
+def test_ring_window_and_long_requests(K, ctx, oracle_mod, pol, flags):
+    """Requests longer than the ring window go through the per-lane long list; an instance
+    with more than 32 of them in flight is rerun by the full-ring launch."""
+    b = _long_batch(400, 40 + pol)
+    many = [([[0, 1, 2100, 2100]] * 40 + [[5, 3, 50, 50], [9, 2, 2500, 2500]], 200000),
+            ([[0, 1, 3000, 3000]] * 33 + [[0, 1, 10, 10]] * 5, 120000)]
+    c = W.from_instances(many)
+    kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=3) if pol >= 2 else {}
+    check(K, ctx, oracle_mod, b, pol, "long requests", flags=flags, **kw)
+    check(K, ctx, oracle_mod, c, pol, "long-list overflow -> full ring", flags=flags, **kw)
+
+
 @pytest.mark.parametrize("pol", [2, 3])
 def test_alpha_with_evictions(K, ctx, oracle_mod, pol):
     """Tight budgets force overflows, evictions and (for alpha-greedy) livelocks."""
