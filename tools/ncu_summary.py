@@ -25,6 +25,22 @@ METRICS = [
 ]
 
 
+POLICY = {"0": "MCSF", "1": "MCBENCH", "2": "ALPHA", "3": "ALPHA_BETA"}
+
+
+def abi_name(short: str) -> str:
+    """ncu's demangled template name -> the name sched_last_kernel() reports."""
+    m = re.match(r"k_mc_small<(\d), (\d), (\d)>", short)
+    if m:
+        pol, multi, qreg = m.groups()
+        tags = [POLICY[pol]] + ([] if multi == "1" else ["per-round"]) + ([] if qreg == "1" else ["smemq"])
+        return "k_mc_small<" + ",".join(tags) + ">"
+    m = re.match(r"k_ring<(\d)>", short)
+    if m:
+        return f"k_ring<{POLICY[m.group(1)]}>"
+    return short
+
+
 def ncu(*args) -> str:
     return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
 
@@ -77,12 +93,12 @@ def main():
         rd = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
         wr = to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
         dur = to_ns(d["gpu__time_duration.sum"], u["gpu__time_duration.sum"])
-        print(f"== {short}")
+        print(f"== {short}  ({abi_name(short)})")
         for m in METRICS:
             if m in d:
                 print(f"  {m:70s} {d[m]:>16s} {u.get(m, '')}")
         print(f"  dram bytes per launch: {rd + wr:.4g}  duration {dur / 1e6:.4f} ms")
-        kernels[short] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+        kernels[abi_name(short)] = {"ncu_name": short, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                           "duration_ms": dur / 1e6, "source": Path(a.rep).name,
                           "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                           "registers": d.get("launch__registers_per_thread"),
