@@ -25,6 +25,10 @@
  *                     is cleared with probability beta, in whole passes until the batch fits
  *                     (DESIGN Q14); draws are Philox4x32-10 on (t, pass, idx, 0) keyed by
  *                     seed ^ (gid * 0x9E3779B97F4A7C15).
+ *   SCHED_MCSF_PROTECTED  MC-SF under prediction error: Algorithm 1 with the
+ *                     possibly wrong predictions o~ against the budget floor((1-alpha)M); when
+ *                     the realised occupancy of a batch exceeds M every active request is
+ *                     cleared and re-queued.
  *
  * Conventions for every entry point.
  *   - Integers only cross the boundary.  All sizes are in KV slots (tokens) and rounds.
@@ -60,7 +64,7 @@ enum {
 };
 
 /* policies (see above) */
-enum { SCHED_MCSF = 0, SCHED_MC_BENCH = 1, SCHED_ALPHA = 2, SCHED_ALPHA_BETA = 3 };
+enum { SCHED_MCSF = 0, SCHED_MC_BENCH = 1, SCHED_ALPHA = 2, SCHED_ALPHA_BETA = 3, SCHED_MCSF_PROTECTED = 4 };
 
 /* per-instance status */
 enum {
@@ -102,8 +106,9 @@ typedef struct {
  * Instances that exceed a caller-given bound get status SCHED_INST_UNSUPPORTED.            */
 
 typedef struct {
-    int32_t policy;             /* SCHED_MCSF .. SCHED_ALPHA_BETA                            */
-    int32_t alpha_num;          /* alpha = alpha_num / alpha_den in [0, 1) (alpha policies);  */
+    int32_t policy;             /* SCHED_MCSF .. SCHED_MCSF_PROTECTED                        */
+    int32_t alpha_num;          /* alpha = alpha_num / alpha_den in [0, 1) (alpha policies and
+                                   SCHED_MCSF_PROTECTED);                                   */
     int32_t alpha_den;          /*   budget B = ((den - num) * M) / den (DESIGN Q15)         */
     int32_t flags;              /* SCHED_FLAG_* bits, 0 = defaults                           */
     uint64_t beta_thresh;       /* alpha-beta: evict iff u32 draw < beta_thresh, in [0, 2^32];

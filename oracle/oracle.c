@@ -19,8 +19,9 @@
  *   or_projected_occupancy  LHS of Eq. 5 at one t'.
  *   or_is_feasible          Eq. 5 for all t' in [t+1, t_max(U)], exhaustive.
  *   or_simulate             one instance, one policy: Alg. 1, Alg. 2
- *                           (P:1076-1103), alpha-protection greedy and
- *                           alpha-protection beta-clearing.
+ *                           (P:1076-1103), alpha-protection greedy,
+ *                           alpha-protection beta-clearing, and MC-SF under
+ *                           prediction error with a protection margin.
  *   or_simulate_batch       or_simulate over a CSR batch with a pthread pool.
  *   or_tel                  TEL = sum_i (c_i - a_i).
  *   or_opt_bruteforce       hindsight optimum of Eqs. 1-4 by exhaustive
@@ -36,6 +37,7 @@
 #define OR_MCBENCH 1     /* Algorithm 2                     */
 #define OR_ALPHA 2       /* alpha-protection greedy           */
 #define OR_ALPHA_BETA 3  /* alpha-protection beta-clearing        */
+#define OR_MCSF_PROT 4   /* MC-SF on (1-alpha)M with clearing */
 
 #define OR_OK 0
 #define OR_INVALID 1
@@ -126,7 +128,7 @@ typedef struct {
 /* R is kept as an array of request indices in the policy's key order. */
 static int or_key_less(const or_inst *I, int policy, int32_t x, int32_t y)
 {
-    if (policy == OR_MCSF) {                       /* (o~, idx): P:143, DESIGN Q5 */
+    if (policy == OR_MCSF || policy == OR_MCSF_PROT) {   /* (o~, idx): P:175, DESIGN Q5 */
         if (I->op[x] != I->op[y]) return I->op[x] < I->op[y];
         return x < y;
     }
@@ -162,7 +164,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
 {
     for (int k = 0; k < 7; k++) stats[k] = 0;
     for (int64_t i = 0; i < n; i++) { completion[i] = -1; if (start) start[i] = -1; }
-    if (policy < OR_MCSF || policy > OR_ALPHA_BETA) return -1;
+    if (policy < OR_MCSF || policy > OR_MCSF_PROT) return -1;
 
     size_t nb = sizeof(int32_t) * (size_t)(n + 2);
     int32_t *a = malloc(nb), *s = malloc(nb), *o = malloc(nb), *op = malloc(nb);
@@ -181,7 +183,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
     int64_t decision_rounds = 0, peak = 0, evictions = 0;
 
     /* ---- instance validation (DESIGN Q8) -------------------------------------------- */
-    if (policy == OR_ALPHA || policy == OR_ALPHA_BETA)
+    if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || policy == OR_MCSF_PROT)
         if (alpha_den <= 0 || alpha_num < 0 || alpha_num >= alpha_den) status = OR_INVALID;
     for (int64_t i = 0; i < n; i++) {
         if (s[i] < 1 || o[i] < 1 || op[i] < 1 || a[i] < 0) status = OR_INVALID;
@@ -191,8 +193,9 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
              * never be admitted (Eq. 5 with S empty fails at t' = t + o~).              */
             if ((int64_t)s[i] + op[i] > M || op[i] < o[i]) status = OR_INVALID;
         } else {
-            /* MC-Benchmark projects with the true o; the alpha policies cannot
-             * ever hold a request whose peak s+o exceeds M.                       */
+            /* MC-Benchmark projects with the true o; the alpha policies and the
+             * protected MC-SF (whose o~ may undershoot) cannot ever hold a request
+             * whose peak s+o exceeds M.                                          */
             if ((int64_t)s[i] + o[i] > M) status = OR_INVALID;
         }
     }
@@ -208,8 +211,12 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
         }
         /* alpha budget B = floor((1 - alpha) M), alpha = num/den (DESIGN Q15) */
         int64_t B = 0;
-        if (policy == OR_ALPHA || policy == OR_ALPHA_BETA)
+        if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || policy == OR_MCSF_PROT)
             B = ((int64_t)(alpha_den - alpha_num) * M) / alpha_den;
+        /* Eq. 5's right-hand side: M, or (1-alpha)M for the protected MC-SF ("run MC-SF as
+         * if the effective budget were (1-alpha)M")                               */
+        const int64_t budget = (policy == OR_MCSF_PROT) ? B : M;
+        const int use_pred = (policy == OR_MCSF || policy == OR_MCSF_PROT);
 
         int64_t nR = 0, nS = 0, next = 0;
         int64_t t = a[0];
@@ -231,19 +238,20 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
             }
             if (nR > 0) decision_rounds++;
 
-            if (policy == OR_MCSF || policy == OR_MCBENCH) {
+            if (policy == OR_MCSF || policy == OR_MCBENCH || policy == OR_MCSF_PROT) {
                 /* Alg. 1 / Alg. 2: walk R in key order, add i
                  * to U while Eq. 5 holds for S and U+{i}; break at the first failure.    */
+                const int64_t idle_before = (nS == 0);
                 for (int64_t k = 0; k < nS; k++) {
                     Ss[k] = s[S[k]]; Sp[k] = p[S[k]];
-                    Sop[k] = (policy == OR_MCSF) ? op[S[k]] : o[S[k]];
+                    Sop[k] = use_pred ? op[S[k]] : o[S[k]];
                 }
                 int64_t nU = 0;
                 for (int64_t k = 0; k < nR; k++) {
                     int32_t i = R[k];
                     Us[nU] = s[i];
-                    Uop[nU] = (policy == OR_MCSF) ? op[i] : o[i];
-                    if (!or_is_feasible(t, M, nS, Ss, Sp, Sop, nU + 1, Us, Uop)) break;
+                    Uop[nU] = use_pred ? op[i] : o[i];
+                    if (!or_is_feasible(t, budget, nS, Ss, Sp, Sop, nU + 1, Us, Uop)) break;
                     U[nU] = i;
                     nU++;
                 }
@@ -256,6 +264,31 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                 }
                 for (int64_t k = 0; k + nU < nR; k++) R[k] = R[k + nU];
                 nR -= nU;
+                if (policy == OR_MCSF_PROT) {
+                    /* an underestimate o~ < o lets the realised KV growth pass M; "such an
+                     * overflow triggers a clearing event, where all active requests are
+                     * evicted and re-queued", with the cycle rule of DESIGN Q24   */
+                    int64_t mem = 0;
+                    for (int64_t k = 0; k < nS; k++) mem += (int64_t)s[S[k]] + t + 1 - p[S[k]];
+                    if (mem > M) {
+                        for (int64_t k = 0; k < nS; k++) {
+                            int32_t j = S[k];
+                            p[j] = -1; c[j] = -1;
+                            or_insert_sorted(&I, policy, R, &nR, j);
+                            evictions++;
+                        }
+                        nS = 0;
+                        if (have_clear && next == next_at_clear && completed_since_clear == 0) {
+                            status = OR_LIVELOCK;
+                            break;
+                        }
+                        have_clear = 1;
+                        next_at_clear = next;
+                        completed_since_clear = 0;
+                    }
+                    /* a head with s + o~ > (1-alpha)M never fits an empty worker */
+                    if (idle_before && nU == 0 && nR > 0) { status = OR_LIVELOCK; break; }
+                }
             } else {
                 /* alpha-protection: FCFS; admit i while the next-round occupancy
                  * of S, plus s+1 for each prompt already admitted, plus s_i+1, stays

@@ -1,0 +1,293 @@
+// kernel_prot.cuh -- MC-SF under prediction error with a protection margin.
+//
+// The scheduler sees noisy predictions o~ (o~ ~ U((1-eps)o, (1+eps)o), integer-
+// rounded on the host), runs Algorithm 1 "as if the effective budget were (1-alpha)M"
+// (P:526), and "an overflow triggers a clearing event, where all active requests are
+// evicted and re-queued".  One warp per instance; two shared-memory rings over the
+// window [t+1, t+L] (plus long-request lists beyond it, see kernel_ring.cuh):
+//   Pp  the projection of Eq. 5: o~-ramps of the requests in S^(t) (an underestimated
+//       request drops out of it once its predicted window ends, the indicator of P:141);
+//   Pa  the realised occupancy of Eq. 3 with the true o (overflow detection, peak).
+// A request that completes before its predicted end (o < o~) leaves S at c = p + o; the
+// unused tail of its projection is removed then.  Such requests are chained per completion
+// round (bucket head per ring slot in shared memory, links in global scratch).
+// Rounds are processed one at a time (idle rounds are jumped).
+#pragma once
+#include "kernel_ring.cuh"
+
+namespace kv {
+
+struct ProtSmem {
+    int *pp;          // [L] projection ring
+    int *pa;          // [L] realised-occupancy ring
+    int *rel;         // [L] early-completion chain heads by completion slot (-1 = empty)
+    uint32_t *bm;     // [NP/32] waiting queue
+    uint32_t *sm;     // [32]
+    uint32_t *infl;   // [NP/32] in-flight set
+};
+
+__host__ __device__ inline int prot_warp_bytes(int L, int NP)
+{
+    int b = 3 * L * 4 + 2 * (NP / 32) * 4 + 32 * 4;
+    return (b + 15) & ~15;
+}
+
+__device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &S)
+{
+    const int lane = lane_id();
+    const long long off = P.offset[inst];
+    const int n = (int)(P.offset[inst + 1] - off);
+    const int M = P.mem[inst];
+    const int L = P.L, mask = L - 1;
+    const int *reqi = reinterpret_cast<const int *>(P.req);
+    InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
+
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem;
+    long long suma = 0, sumo = 0;
+    if (!unsup) {
+        for (int k = lane; k < n; k += 32) {
+            const int4 r = P.req[off + k];
+            bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
+            if (k > 0) bad |= reqi[(off + k - 1) * 4] > r.x;
+            bad |= (long long)r.y + r.z > M;                    // physically feasible
+            unsup |= r.z > P.max_len || r.w > P.max_len;
+            suma += r.x;
+            sumo += r.z;
+        }
+    }
+    bad = __any_sync(KV_FULL, bad);
+    unsup = __any_sync(KV_FULL, unsup);
+    suma = warp_sum_i64(suma);
+    sumo = warp_sum_i64(sumo);
+    if (unsup || bad) {
+        res.status = unsup ? ST_UNSUPPORTED : ST_INVALID;
+        fill_unscheduled(P, off, n);
+        write_result(P, inst, res);
+        return;
+    }
+    if (n == 0) { write_result(P, inst, res); return; }
+
+    const int NPi = next_pow2(max(n, 32));
+    const int nw = NPi >> 5;
+    for (int i = lane; i < L; i += 32) { S.pp[i] = 0; S.pa[i] = 0; S.rel[i] = -1; }
+    for (int w = lane; w < nw; w += 32) { S.bm[w] = 0u; S.infl[w] = 0u; }
+    S.sm[lane] = 0u;
+    __syncwarp();
+    WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
+
+    const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
+    const int cap = (int)min(cap64, 0x7ffffffell);
+    const int B = (int)(((long long)(P.alpha_den - P.alpha_num) * M) / P.alpha_den);   // (1-alpha)M
+    int *relnext = P.relnext + off;                     // chain links by idx
+    int *pst = P.pstart + off;                          // start rounds by idx
+
+    int t = reqi[off * 4];
+    int next = 0, a_next = t;
+    int h = KV_INF;
+    uint4 he = make_uint4(0, 0, 0, 0);
+    bool hstale = false;
+    long long sumc = 0, evictions = 0;
+    int rounds = 0, drounds = 0, peak = 0, status = ST_OK, mem_prev = 0;
+    int adm_since_clear = 0, next_at_clear = -1;     // cycle rule (DESIGN Q24)
+    LongList Gp, Ga;
+    Gp.p = Gp.s = Gp.e = Gp.idx = 0;
+    Gp.used = 0u;
+    Ga = Gp;
+
+    for (;;) {
+        if (h == KV_INF && mem_prev == 0) {               // R and S empty: idle jump
+            if (a_next == KV_INF) break;
+            t = max(t, a_next);                           // rings and long lists are empty
+        }
+        if (t > cap) { status = ST_LIVELOCK; break; }
+
+        while (a_next <= t) {                             // arrivals
+            const int k = next + lane;
+            const int ak = k < n ? reqi[(off + k) * 4] : KV_INF;
+            const bool take = ak <= t;
+            const int cnt = __popc(__ballot_sync(KV_FULL, take));
+            int rk = KV_INF;
+            if (take) {
+                rk = P.arank[off + k];
+                q_insert(Q, rk);
+            }
+            const int mn = warp_min_i32(rk);
+            if (mn < h) { h = mn; hstale = true; }
+            next += cnt;
+            a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? reqi[(off + next) * 4] : KV_INF);
+        }
+        __syncwarp();
+
+        // completions before the predicted end (o < o~): the request leaves S^(t), so its
+        // projection beyond t drops out of Eq. 5
+        {
+            int prev = -1, cur = S.rel[t & mask];
+            while (cur >= 0) {
+                const int nxt = relnext[cur];
+                const int p_ = pst[cur];
+                const int o_ = reqi[(off + cur) * 4 + 2];
+                if (p_ + o_ == t) {
+                    const int s_ = reqi[(off + cur) * 4 + 1], w_ = reqi[(off + cur) * 4 + 3];
+                    ring_ramp(S.pp, mask, t, min(p_ + w_ - t, L), s_ + t - p_, -1);
+                    if (p_ + w_ > t + L) long_remove_idx(Gp, cur);
+                    __syncwarp();
+                    if (lane == 0) { if (prev < 0) S.rel[t & mask] = nxt; else relnext[prev] = nxt; }
+                } else {
+                    prev = cur;                            // a later completion on the same slot
+                }
+                __syncwarp();
+                cur = nxt;
+            }
+        }
+        __syncwarp();
+
+        const bool had_R = h != KV_INF;
+        const bool idle_before = S.pa[(t + 1) & mask] == 0;
+        int admitted = 0;
+        if (had_R) {
+            ++drounds;
+            if (hstale) { he = P.rq[off + h]; hstale = false; }
+            for (;;) {                                     // Alg. 1 on budget (1-alpha)M
+                const int s = (int)he.x, w = (int)he.y, o = (int)he.z, idx = (int)he.w;
+                bool viol = false;
+                for (int base = 1; base <= w; base += 32) {
+                    const int tau = base + lane;
+                    const int v = prof_at(S.pp, mask, L, Gp, t, tau);
+                    viol |= tau <= w && v + s + tau > B;
+                }
+                if (__any_sync(KV_FULL, viol)) break;
+                if (!ring_admit(S.pp, mask, L, Gp, t, w, s, idx) || !ring_admit(S.pa, mask, L, Ga, t, o, s, idx)) {
+                    status = ST_RETRY;
+                    break;
+                }
+                const int c = t + o;
+                if (lane == 0) {
+                    if (P.completion) P.completion[off + idx] = c;
+                    if (P.start) P.start[off + idx] = t;
+                    pst[idx] = t;
+                    S.infl[idx >> 5] |= 1u << (idx & 31);
+                    if (w > o) { relnext[idx] = S.rel[c & mask]; S.rel[c & mask] = idx; }
+                }
+                sumc += c;
+                ++admitted;
+                ++adm_since_clear;
+                __syncwarp();
+                h = q_pop_head(Q, h);
+                if (h == KV_INF) break;
+                he = P.rq[off + h];
+            }
+            if (status == ST_RETRY) break;
+        }
+        __syncwarp();
+
+        // realised overflow: clear every active request
+        bool cycle = false;
+        if (S.pa[(t + 1) & mask] > M) {
+            long long ev = 0;
+            for (int wb = 0; wb < nw; wb += 32) {
+                const int wi = wb + lane;
+                uint32_t bits = wi < nw ? S.infl[wi] : 0u;
+                while (__any_sync(KV_FULL, bits != 0u)) {
+                    int j = -1;
+                    bool act = false;
+                    if (bits) {
+                        j = (wi << 5) + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        act = pst[j] + reqi[(off + j) * 4 + 2] > t;
+                    }
+                    const uint32_t am = __ballot_sync(KV_FULL, act);
+                    if (am) {
+                        ev += __popc(am);
+                        sumc -= warp_sum_i64(act ? (long long)(pst[j] + reqi[(off + j) * 4 + 2]) : 0ll);
+                        if (act) {
+                            q_insert(Q, (int)P.arank[off + j]);
+                            if (P.completion) P.completion[off + j] = -1;
+                            if (P.start) P.start[off + j] = -1;
+                        }
+                    }
+                }
+                if (wi < nw) S.infl[wi] = 0u;
+            }
+            // the head is a rank: recompute it over the re-queued set
+            __syncwarp();
+            h = q_first(Q);
+            hstale = h != KV_INF;
+            for (int i = lane; i < L; i += 32) { S.pp[i] = 0; S.pa[i] = 0; S.rel[i] = -1; }
+            Gp.used = 0u;
+            Ga.used = 0u;
+            __syncwarp();
+            evictions += ev;
+            cycle = next_at_clear == next && ev == adm_since_clear;
+            next_at_clear = next;
+            adm_since_clear = 0;
+        }
+        if (cycle) { status = ST_LIVELOCK; break; }
+        if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
+        if (had_R || !idle_before) ++rounds;
+        const int mnow = ring_jump(S.pa, mask, L, Ga, t, t + 1, t + 1);   // Mem(t+1)
+        ring_jump(S.pp, mask, L, Gp, t, t, t + 1);
+        peak = max(peak, mnow);
+        mem_prev = mnow;
+        ++t;
+    }
+
+    if (status == ST_RETRY) {
+        if (lane == 0) P.retry_list[atomicAdd(P.retry_count, 1ull)] = inst;
+        return;
+    }
+    if (status != ST_OK) {
+        for (int k = next + lane; k < n; k += 32) {
+            if (P.completion) P.completion[off + k] = -1;
+            if (P.start) P.start[off + k] = -1;
+        }
+        for (int w = lane; w < nw; w += 32) {
+            uint32_t bits = S.bm[w];
+            while (bits) {
+                const int r = (w << 5) + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int idx = (int)P.rq[off + r].w;
+                if (P.completion) P.completion[off + idx] = -1;
+                if (P.start) P.start[off + idx] = -1;
+            }
+        }
+    }
+    int mx = -1;
+    if (status == ST_OK)
+        for (int k = lane; k < n; k += 32) mx = max(mx, pst[k] + reqi[(off + k) * 4 + 2]);
+    res.tel = sumc - suma;
+    res.rounds = rounds;
+    res.decision_rounds = drounds;
+    res.evictions = evictions;
+    res.makespan = warp_max_i32(mx);
+    res.peak = peak;
+    res.status = status;
+    write_result(P, inst, res);
+}
+
+__global__ void __launch_bounds__(128) k_prot(const KParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *base = smem_raw + (size_t)warp * P.warp_bytes;
+    ProtSmem S;
+    S.pp = reinterpret_cast<int *>(base);
+    S.pa = S.pp + P.L;
+    S.rel = S.pa + P.L;
+    S.bm = reinterpret_cast<uint32_t *>(S.rel + P.L);
+    S.infl = S.bm + P.NP / 32;
+    S.sm = S.infl + P.NP / 32;
+
+    const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+    long long w = 0;
+    if (lane == 0) w = atomicAdd(P.counter, 1ull);
+    w = __shfl_sync(KV_FULL, w, 0);
+    while (w < n_work) {
+        long long nxt = 0;
+        if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
+        prot_instance(P, P.work_list ? P.work_list[w] : w, S);
+        w = __shfl_sync(KV_FULL, nxt, 0);
+        __syncwarp();
+    }
+}
+
+}  // namespace kv

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/kvsched.h"
+#include "kernel_prot.cuh"
 #include "kernel_ring.cuh"
 #include "kernel_small.cuh"
 
@@ -39,7 +40,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, total, retry;
+    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -229,7 +230,7 @@ int check_common(sched_ctx *c, const sched_instances *inst)
 int check_policy(sched_ctx *c, const sched_policy *pol)
 {
     if (!pol) return fail(c, SCHED_E_ARG, "pol is NULL");
-    if (pol->policy < SCHED_MCSF || pol->policy > SCHED_ALPHA_BETA)
+    if (pol->policy < SCHED_MCSF || pol->policy > SCHED_MCSF_PROTECTED)
         return fail(c, SCHED_E_ARG, "unknown policy %d", pol->policy);
     if (pol->flags & ~SCHED_FLAG_PER_ROUND) return fail(c, SCHED_E_ARG, "unknown flags 0x%x", pol->flags);
     if (pol->policy >= SCHED_ALPHA) {
@@ -381,17 +382,19 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     const int L_full = next_pow2(max_len + 33);
     const int L_short = L_full < KV_RING_SHORT ? L_full : KV_RING_SHORT;
     P.L = L_short;
-    P.warp_bytes = ring_warp_bytes(P.L, P.NP, pol->policy);
-    if ((size_t)ring_warp_bytes(L_full, P.NP, pol->policy) > c->max_smem_optin)
+    const bool prot = pol->policy == SCHED_MCSF_PROTECTED;
+    auto wbytes = [&](int L) { return prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy); };
+    P.warp_bytes = wbytes(P.L);
+    if ((size_t)wbytes(L_full) > c->max_smem_optin)
         return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
-                    ring_warp_bytes(L_full, P.NP, pol->policy), L_full, P.NP);
+                    wbytes(L_full), L_full, P.NP);
     if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
     P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
     P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
     CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
     const size_t slots = (size_t)inst->n_instances * (size_t)max_req;
     const char *name = "";
-    if (pol->policy == SCHED_MCSF) {
+    if (pol->policy == SCHED_MCSF || prot) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
         // offsets are relative to the batch: scratch slot = request row (n_req <= slots)
         P.rq = reinterpret_cast<const uint4 *>(c->rq.p);
@@ -403,15 +406,21 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
                                                              reinterpret_cast<int *>(c->arank.p));
         CUDA_TRY(c, cudaGetLastError());
         c->launches++;
-    } else if (pol->policy >= SCHED_ALPHA) {
+    }
+    if (pol->policy >= SCHED_ALPHA) {
         if ((rc = grow(c, c->pstart, slots * 4))) return rc;
         P.pstart = reinterpret_cast<int *>(c->pstart.p);
+    }
+    if (prot) {
+        if ((rc = grow(c, c->relnext, slots * 4))) return rc;
+        P.relnext = reinterpret_cast<int *>(c->relnext.p);
     }
     auto launch_ring = [&](const KParams &Q) -> int {
         switch (pol->policy) {
         case SCHED_MCSF: name = "k_ring<MCSF>"; return launch_sim(c, k_ring<POL_MCSF>, Q, Q.warp_bytes, name);
         case SCHED_MC_BENCH: name = "k_ring<MCBENCH>"; return launch_sim(c, k_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);
         case SCHED_ALPHA: name = "k_ring<ALPHA>"; return launch_sim(c, k_ring<POL_ALPHA>, Q, Q.warp_bytes, name);
+        case SCHED_MCSF_PROTECTED: name = "k_prot<MCSF_PROTECTED>"; return launch_sim(c, k_prot, Q, Q.warp_bytes, name);
         default: name = "k_ring<ALPHA_BETA>"; return launch_sim(c, k_ring<POL_ALPHA_BETA>, Q, Q.warp_bytes, name);
         }
     };
@@ -419,7 +428,7 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     if (L_short < L_full) {
         KParams Q = P;
         Q.L = L_full;
-        Q.warp_bytes = ring_warp_bytes(L_full, P.NP, pol->policy);
+        Q.warp_bytes = wbytes(L_full);
         Q.work_list = P.retry_list;
         Q.work_count = P.retry_count;
         Q.retry_list = nullptr;          // the full ring never overflows (no long requests)
@@ -562,7 +571,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->total, &c->retry, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {

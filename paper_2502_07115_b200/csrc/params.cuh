@@ -5,7 +5,7 @@
 
 namespace kv {
 
-enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3 };
+enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3, POL_MCSF_PROT = 4 };
 enum { ST_OK = 0, ST_INVALID = 1, ST_LIVELOCK = 2, ST_UNSUPPORTED = 3, ST_RETRY = 4 /* internal */ };
 
 struct KParams {
@@ -31,6 +31,7 @@ struct KParams {
     // scratch
     unsigned long long *counter; // persistent-grid work counter (zeroed before launch)
     int *pstart;                // alpha policies: start round of each request (scratch)
+    int *relnext;               // protected MC-SF: early-completion chain links (scratch)
     const uint4 *rq;            // MC-SF ring path: per-rank entries {s, o~, o, idx}
     const int *arank;           // MC-SF ring path: rank of request idx
     long long *retry_list;      // ring kernel: instances handed to the full-ring launch

@@ -15,8 +15,9 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libkvsched.so"
 
-MCSF, MC_BENCH, ALPHA, ALPHA_BETA = 0, 1, 2, 3
-POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": ALPHA_BETA}
+MCSF, MC_BENCH, ALPHA, ALPHA_BETA, MCSF_PROTECTED = 0, 1, 2, 3, 4
+POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": ALPHA_BETA,
+              "mcsf_protected": MCSF_PROTECTED}
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}

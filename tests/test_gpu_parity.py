@@ -15,7 +15,7 @@ import workloads as W
 pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-KIND = {0: "mcsf", 1: "mcbench", 2: "alpha", 3: "alpha_beta"}
+KIND = {0: "mcsf", 1: "mcbench", 2: "alpha", 3: "alpha_beta", 4: "mcsf_protected"}
 
 
 @pytest.fixture(scope="module")
@@ -210,6 +210,20 @@ def test_ring_window_and_long_requests(K, ctx, oracle_mod, pol, flags):
     kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=3) if pol >= 2 else {}
     check(K, ctx, oracle_mod, b, pol, "long requests", flags=flags, **kw)
     check(K, ctx, oracle_mod, c, pol, "long-list overflow -> full ring", flags=flags, **kw)
+
+
+@pytest.mark.parametrize("eps", [0.2, 0.5, 0.8])
+@pytest.mark.parametrize("shape", ["small", "long", "c4"])
+def test_protected_mcsf(K, ctx, oracle_mod, eps, shape):
+    """NEXT-1: noisy predictions, budget (1-alpha)M, clearing on overflow."""
+    b = {"small": lambda: W.random_small(2000, 50, n_max=40, M_lo=10, M_hi=80, a_max=30),
+         "long": lambda: _long_batch(300, 51),
+         "c4": lambda: W.c4(32, 52)}[shape]()
+    b = W.with_prediction_noise(b, eps, seed=53)
+    for alpha in ((1, 10), (0, 1)):
+        o, g = check(K, ctx, oracle_mod, b, 4, f"protected eps={eps} alpha={alpha}", alpha=alpha)
+    if shape == "small":
+        assert o["evictions"].sum() > 0
 
 
 @pytest.mark.parametrize("pol", [2, 3])

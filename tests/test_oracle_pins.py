@@ -374,3 +374,67 @@ def test_policy_ordering_table1_shape(oracle_mod):
     for name in means:
         if name.startswith("alpha"):
             assert means["MC-Benchmark"] < means[name]
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-1: MC-SF under prediction error with a protection margin
+# ----------------------------------------------------------------------------------------
+def test_protected_mcsf_reduces_to_mcsf(oracle_mod):
+    """alpha = 0 and o^ >= o: the projection never underestimates, nothing overflows, so
+    the protected variant is Algorithm 1 with o~ = o^."""
+    O = oracle_mod
+    b = W.random_small(120, 91, n_max=25, M_lo=8, M_hi=60, a_max=20, pred_slack=5)
+    for k in range(b.n_inst):
+        req, M = b.instance(k)
+        x, y = O.simulate(req, M, O.MCSF), O.simulate(req, M, O.MCSF_PROT, alpha=(0, 1))
+        for key in ("completion", "tel", "status", "peak", "decision_rounds"):
+            assert np.array_equal(np.asarray(x[key]), np.asarray(y[key]))
+        assert y["evictions"] == 0
+
+
+def test_protected_mcsf_overflow_worked_example(oracle_mod):
+    """Two (s=1, o=6) requests predicted o^=2, M=10, alpha=0: both start at 0 (projection
+    peaks at 6); the realised memory reaches 10 at t=4 and 12 at t=5, so round 4 clears
+    both; re-admitted at 5, cleared again at 9 with nothing completed or arrived:
+    the cycle repeats for ever (DESIGN Q24).  With a third request arriving at 7 the second
+    clear is not a repeat; the third clear at 11 is."""
+    O = oracle_mod
+    r = O.simulate([[0, 1, 6, 2], [0, 1, 6, 2]], 10, O.MCSF_PROT, alpha=(0, 1))
+    assert (r["status"], r["decision_rounds"], r["evictions"], r["peak"]) == (2, 2, 4, 10)
+    r = O.simulate([[0, 1, 6, 2], [0, 1, 6, 2], [7, 1, 3, 3]], 10, O.MCSF_PROT, alpha=(0, 1))
+    assert (r["status"], r["decision_rounds"], r["evictions"], r["peak"]) == (2, 4, 8, 10)
+    # alpha = 0.5 (budget 5): A starts at 0; B fails at t=1? no -- A's projection ends at
+    # t'=2 (o^=2), so at t=1 B's window sees 3+2=5 at t'=2 and 3 at t'=3: B starts at 1.
+    # Realised Mem(5) = 6 + 5 = 11 > 10 at t=4: clear; A at 5, B at 6, clear at 9 (repeat).
+    # Decision rounds t = 0, 1, 5, 6; peak Mem(4) = 5 + 4 = 9.
+    r = O.simulate([[0, 1, 6, 2], [0, 1, 6, 2]], 10, O.MCSF_PROT, alpha=(1, 2))
+    assert (r["status"], r["decision_rounds"], r["evictions"], r["peak"]) == (2, 4, 4, 9)
+
+
+@pytest.mark.parametrize("eps", [0.2, 0.5, 0.8])
+def test_protected_mcsf_schedules_valid(oracle_mod, eps):
+    """Every completed protected-MC-SF schedule respects the model (p >= a, c = p + o,
+    memory <= M every round): clearing removes any batch that would overflow."""
+    O = oracle_mod
+    b = W.with_prediction_noise(W.random_small(120, 92, n_max=25, M_lo=10, M_hi=60, a_max=20), eps)
+    n_ev = 0
+    for k in range(b.n_inst):
+        req, M = b.instance(k)
+        out = O.simulate(req, M, O.MCSF_PROT, alpha=(1, 10))
+        n_ev += out["evictions"]
+        if out["status"] == 0 and len(req):
+            check_schedule(req, M, out)
+    assert n_ev > 0
+
+
+def test_protected_mcsf_unconstrained(oracle_mod):
+    """Budget large enough for every projection and every realised batch: c = a + o."""
+    O = oracle_mod
+    b = W.with_prediction_noise(W.random_small(60, 93, n_max=12, M_lo=4, M_hi=30), 0.8)
+    for k in range(b.n_inst):
+        req, _ = b.instance(k)
+        if len(req) == 0:
+            continue
+        M = int(2 * (req[:, 1] + np.maximum(req[:, 2], req[:, 3])).sum())
+        out = O.simulate(req, M, O.MCSF_PROT, alpha=(1, 2))
+        assert out["status"] == 0 and (out["completion"] == req[:, 0] + req[:, 2]).all()
