@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--impl", default="kvsched", choices=["kvsched", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4", "c3"])
     ap.add_argument("--instances", type=int, default=0, help="instances per GPU (0 = config size)")
-    ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta"])
+    ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta", "mcsf_protected"])
+    ap.add_argument("--eps", type=float, default=0.2, help="prediction noise for mcsf_protected (P:519)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -79,6 +80,8 @@ def policy_of(K, name):
         return K.Policy("alpha", (1, 4))
     if name == "alpha_beta":
         return K.Policy("alpha_beta", (1, 5), W.beta_threshold(0.1), seed=1)
+    if name == "mcsf_protected":
+        return K.Policy("mcsf_protected", (1, 10))
     return K.Policy(name)
 
 
@@ -86,7 +89,8 @@ def oracle_policy(name):
     import oracle
     return {"mcsf": (oracle.MCSF, {}), "mcbench": (oracle.MCBENCH, {}),
             "alpha": (oracle.ALPHA, dict(alpha=(1, 4))),
-            "alpha_beta": (oracle.ALPHA_BETA, dict(alpha=(1, 5), beta_thresh=W.beta_threshold(0.1), seed=1))}[name]
+            "alpha_beta": (oracle.ALPHA_BETA, dict(alpha=(1, 5), beta_thresh=W.beta_threshold(0.1), seed=1)),
+            "mcsf_protected": (oracle.MCSF_PROT, dict(alpha=(1, 10)))}[name]
 
 
 def cpu_oracle_rate(batch, policy: str, seconds: float, gid0: int = 0):
@@ -126,7 +130,7 @@ class Clocks:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -201,6 +205,9 @@ def run_reference(args):
     if rank != 0:
         return 0
     batch, cfg = make_workload(args.workload, args.instances, 0)
+    if args.policy == "mcsf_protected":
+        batch = W.with_prediction_noise(batch, args.eps, seed=7)
+        cfg["prediction_noise_eps"] = args.eps
     per_step = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
     for _ in range(args.warmup):
         cpu_oracle_rate(batch, args.policy, per_step)
@@ -237,6 +244,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     batch, cfg = make_workload(args.workload, args.instances, rank)
+    if args.policy == "mcsf_protected":
+        batch = W.with_prediction_noise(batch, args.eps, seed=7 + rank)
+        cfg["prediction_noise_eps"] = args.eps
     hints = K.hints_of(batch)
     off, req, mem = K.to_device(batch, dev)
     fields = K.kvsched.OUT_FIELDS

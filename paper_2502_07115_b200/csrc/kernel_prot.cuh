@@ -35,8 +35,8 @@ __host__ __device__ inline int prot_warp_bytes(int L, int NP)
 __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &S)
 {
     const int lane = lane_id();
-    const long long off = P.offset[inst];
-    const int n = (int)(P.offset[inst + 1] - off);
+    const long long off = P.offset[inst] - P.row_base;      // row of request 0
+    const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
     const int M = P.mem[inst];
     const int L = P.L, mask = L - 1;
     const int *reqi = reinterpret_cast<const int *>(P.req);

@@ -164,8 +164,8 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
 {
     constexpr bool MC = POL == POL_MCSF || POL == POL_MCBENCH;
     const int lane = lane_id();
-    const long long off = P.offset[inst];
-    const int n = (int)(P.offset[inst + 1] - off);
+    const long long off = P.offset[inst] - P.row_base;      // row of request 0
+    const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
     const int M = P.mem[inst];
     const int L = P.L, mask = L - 1;
     const int *reqi = reinterpret_cast<const int *>(P.req);
@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(1024) k_rank_sort(const KParams P, uint4 *rq, 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem_raw);
     for (long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {
-        const long long off = P.offset[inst];
-        const int n = (int)(P.offset[inst + 1] - off);
+        const long long off = P.offset[inst] - P.row_base;
+        const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
         if (n <= 0 || n > P.max_requests) continue;
         const int NPi = next_pow2(n);
         for (int k = threadIdx.x; k < NPi; k += blockDim.x) {

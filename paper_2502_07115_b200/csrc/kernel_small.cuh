@@ -188,8 +188,8 @@ template <int POL, bool MULTI, class Queue>
 __device__ void small_instance(const KParams &P, long long inst, const SmallSmem &S)
 {
     const int lane = lane_id();
-    const long long off = P.offset[inst];
-    const int n = (int)(P.offset[inst + 1] - off);
+    const long long off = P.offset[inst] - P.row_base;      // row of request 0
+    const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
     const int M = P.mem[inst];
     InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
 

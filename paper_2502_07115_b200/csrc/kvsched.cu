@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -48,6 +49,8 @@ struct sched_ctx {
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     std::vector<cudaEvent_t> free_events;
+    cudaStream_t s_in = nullptr, s_out = nullptr;     // host path copy streams
+    std::vector<cudaEvent_t> chunk_events;
 };
 
 static char g_init_err[512];
@@ -290,15 +293,15 @@ int sched_set_stream(sched_ctx *c, void *cuda_stream)
     return SCHED_OK;
 }
 
-int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
-                        const sched_outputs *out)
+}  // extern "C"
+
+// Device-pointer run.  Request rows of instance k start at req_offset[k] - row_base in
+// `req` (and in the completion / start outputs): row_base lets the pipelined host path run
+// chunks whose rows sit in chunk-local buffers while the offsets stay global.
+static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
+                    const sched_outputs *out, long long row_base)
 {
-    int rc = check_common(c, inst);
-    if (rc) return rc;
-    if ((rc = check_policy(c, pol))) return rc;
-    if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
-    if (inst->n_instances == 0) return SCHED_OK;
-    DeviceGuard g(c->device);
+    int rc = SCHED_OK;
 
     int max_req = inst->max_requests, max_mem = inst->max_mem, max_len = inst->max_len;
     if (max_req == 0 || max_mem == 0 || max_len == 0) {
@@ -326,6 +329,7 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     KParams P;
     memset(&P, 0, sizeof(P));
     P.n_inst = inst->n_instances;
+    P.row_base = row_base;
     P.offset = reinterpret_cast<const long long *>(inst->req_offset);
     P.req = reinterpret_cast<const int4 *>(inst->req);
     P.mem = inst->mem_limit;
@@ -439,6 +443,23 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     return SCHED_OK;
 }
 
+extern "C" {
+
+int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
+                        const sched_outputs *out)
+{
+    int rc = check_common(c, inst);
+    if (rc) return rc;
+    if ((rc = check_policy(c, pol))) return rc;
+    if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
+    if (inst->n_instances == 0) return SCHED_OK;
+    DeviceGuard g(c->device);
+    return run_impl(c, inst, pol, out, 0);
+}
+
+// Host buffers.  The batch is cut into chunks of whole instances; chunk k's request rows are
+// copied in on one stream, simulated on the context's stream, and its outputs copied out on
+// a third, so the PCIe transfers of neighbouring chunks overlap the kernels.
 int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
                              const sched_outputs *out)
 {
@@ -449,8 +470,30 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     const long long ni = inst->n_instances;
     if (ni == 0) return SCHED_OK;
     DeviceGuard g(c->device);
-    const long long n_req = inst->req_offset[ni];
-    if (n_req < 0) return fail(c, SCHED_E_ARG, "req_offset[n] < 0");
+    const int64_t *hoff = inst->req_offset;
+    const long long n_req = hoff[ni];
+    if (n_req < 0 || hoff[0] != 0) return fail(c, SCHED_E_ARG, "req_offset must start at 0 and end >= 0");
+    // size hints on the host (the offsets and budgets are host memory here)
+    sched_instances hi = *inst;
+    if (hi.max_requests == 0 || hi.max_mem == 0 || hi.max_len == 0) {
+        long long mr = 0, mm = 0, ml = 0;
+        for (long long k = 0; k < ni; ++k) {
+            mr = hoff[k + 1] - hoff[k] > mr ? hoff[k + 1] - hoff[k] : mr;
+            mm = inst->mem_limit[k] > mm ? inst->mem_limit[k] : mm;
+        }
+        if (hi.max_len == 0)
+            for (long long i = 0; i < n_req; ++i) {
+                const int32_t *r = inst->req + 4 * i;
+                ml = r[2] > ml ? r[2] : ml;
+                ml = r[3] > ml ? r[3] : ml;
+            }
+        if (hi.max_requests == 0) hi.max_requests = (int32_t)(mr < 0x7fffffff ? mr : 0x7fffffff);
+        if (hi.max_mem == 0) hi.max_mem = (int32_t)mm;
+        if (hi.max_len == 0) hi.max_len = (int32_t)(ml < 0x7fffffff ? ml : 0x7fffffff);
+        if (hi.max_requests == 0) hi.max_requests = 1;
+        if (hi.max_mem == 0) hi.max_mem = 1;
+        if (hi.max_len == 0) hi.max_len = 1;
+    }
     const size_t b_off = (size_t)(ni + 1) * 8, b_req = (size_t)n_req * 16, b_mem = (size_t)ni * 4;
     if ((rc = grow(c, c->h_off, b_off)) || (rc = grow(c, c->h_req, b_req)) || (rc = grow(c, c->h_mem, b_mem)))
         return rc;
@@ -460,32 +503,67 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     const size_t total = o_i32 + (size_t)ni * 4 * 3;
     if ((rc = grow(c, c->h_out, total))) return rc;
     char *ob = (char *)c->h_out.p;
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_off.p, inst->req_offset, b_off, cudaMemcpyHostToDevice, c->stream));
-    if (b_req) CUDA_TRY(c, cudaMemcpyAsync(c->h_req.p, inst->req, b_req, cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_mem.p, inst->mem_limit, b_mem, cudaMemcpyHostToDevice, c->stream));
-    sched_instances di = *inst;
-    di.req_offset = (const int64_t *)c->h_off.p;
-    di.req = (const int32_t *)c->h_req.p;
-    di.mem_limit = (const int32_t *)c->h_mem.p;
-    sched_outputs dout;
-    dout.completion = out->completion ? (int32_t *)(ob + o_comp) : nullptr;
-    dout.start = out->start ? (int32_t *)(ob + o_start) : nullptr;
-    dout.tel = out->tel ? (int64_t *)(ob + o_i64) : nullptr;
-    dout.rounds = out->rounds ? (int64_t *)(ob + o_i64 + ni * 8) : nullptr;
-    dout.decision_rounds = out->decision_rounds ? (int64_t *)(ob + o_i64 + ni * 16) : nullptr;
-    dout.evictions = out->evictions ? (int64_t *)(ob + o_i64 + ni * 24) : nullptr;
-    dout.makespan = out->makespan ? (int32_t *)(ob + o_i32) : nullptr;
-    dout.peak_mem = out->peak_mem ? (int32_t *)(ob + o_i32 + ni * 4) : nullptr;
-    dout.status = out->status ? (int32_t *)(ob + o_i32 + ni * 8) : nullptr;
-    if ((rc = sched_run_instances(c, &di, pol, &dout))) return rc;
-    struct { void *h; const void *d; size_t b; } cp[] = {
-        {out->completion, dout.completion, (size_t)n_req * 4}, {out->start, dout.start, (size_t)n_req * 4},
-        {out->tel, dout.tel, (size_t)ni * 8}, {out->rounds, dout.rounds, (size_t)ni * 8},
-        {out->decision_rounds, dout.decision_rounds, (size_t)ni * 8}, {out->evictions, dout.evictions, (size_t)ni * 8},
-        {out->makespan, dout.makespan, (size_t)ni * 4}, {out->peak_mem, dout.peak_mem, (size_t)ni * 4},
-        {out->status, dout.status, (size_t)ni * 4}};
-    for (auto &x : cp)
-        if (x.h && x.b) CUDA_TRY(c, cudaMemcpyAsync(x.h, x.d, x.b, cudaMemcpyDeviceToHost, c->stream));
+    if (!c->s_in) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+    }
+    // chunks of ~4 M request rows (64 MB), at most 32 (KVSCHED_HOST_CHUNK_ROWS overrides the
+    // chunk size; used by the tests to exercise the pipeline on small batches)
+    long long chunk_rows = 4ll << 20;
+    if (const char *e = getenv("KVSCHED_HOST_CHUNK_ROWS")) chunk_rows = atoll(e) > 0 ? atoll(e) : chunk_rows;
+    long long n_chunks = n_req / chunk_rows;
+    if (n_chunks < 1) n_chunks = 1;
+    if (n_chunks > 256) n_chunks = 256;
+    if (n_chunks > ni) n_chunks = ni;
+    while ((long long)c->chunk_events.size() < 2 * n_chunks + 1) c->chunk_events.push_back(take_event(c));
+    cudaEvent_t *ev = c->chunk_events.data();
+    // the previous work on the context's stream precedes every copy of this call
+    CUDA_TRY(c, cudaEventRecord(ev[2 * n_chunks], c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s_in, ev[2 * n_chunks], 0));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_off.p, hoff, b_off, cudaMemcpyHostToDevice, c->s_in));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_mem.p, inst->mem_limit, b_mem, cudaMemcpyHostToDevice, c->s_in));
+    const long long *doff = (const long long *)c->h_off.p;
+    for (long long k = 0; k < n_chunks; ++k) {
+        const long long i0 = ni * k / n_chunks, i1 = ni * (k + 1) / n_chunks;
+        const long long r0 = hoff[i0], r1 = hoff[i1];
+        if (r1 > r0)
+            CUDA_TRY(c, cudaMemcpyAsync((char *)c->h_req.p + r0 * 16, inst->req + 4 * r0, (size_t)(r1 - r0) * 16,
+                                        cudaMemcpyHostToDevice, c->s_in));
+        CUDA_TRY(c, cudaEventRecord(ev[2 * k], c->s_in));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2 * k], 0));
+        sched_instances di = hi;
+        di.n_instances = i1 - i0;
+        di.req_offset = (const int64_t *)(doff + i0);
+        di.req = (const int32_t *)((char *)c->h_req.p + r0 * 16);
+        di.mem_limit = (const int32_t *)c->h_mem.p + i0;
+        di.instance_id0 = inst->instance_id0 + i0;
+        sched_outputs dout;
+        dout.completion = out->completion ? (int32_t *)(ob + o_comp) + r0 : nullptr;
+        dout.start = out->start ? (int32_t *)(ob + o_start) + r0 : nullptr;
+        dout.tel = out->tel ? (int64_t *)(ob + o_i64) + i0 : nullptr;
+        dout.rounds = out->rounds ? (int64_t *)(ob + o_i64 + ni * 8) + i0 : nullptr;
+        dout.decision_rounds = out->decision_rounds ? (int64_t *)(ob + o_i64 + ni * 16) + i0 : nullptr;
+        dout.evictions = out->evictions ? (int64_t *)(ob + o_i64 + ni * 24) + i0 : nullptr;
+        dout.makespan = out->makespan ? (int32_t *)(ob + o_i32) + i0 : nullptr;
+        dout.peak_mem = out->peak_mem ? (int32_t *)(ob + o_i32 + ni * 4) + i0 : nullptr;
+        dout.status = out->status ? (int32_t *)(ob + o_i32 + ni * 8) + i0 : nullptr;
+        if (di.n_instances > 0 && (rc = run_impl(c, &di, pol, &dout, r0))) return rc;
+        CUDA_TRY(c, cudaEventRecord(ev[2 * k + 1], c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, ev[2 * k + 1], 0));
+        struct { void *h; const void *d; size_t b; } cp[] = {
+            {out->completion ? out->completion + r0 : nullptr, dout.completion, (size_t)(r1 - r0) * 4},
+            {out->start ? out->start + r0 : nullptr, dout.start, (size_t)(r1 - r0) * 4},
+            {out->tel ? out->tel + i0 : nullptr, dout.tel, (size_t)(i1 - i0) * 8},
+            {out->rounds ? out->rounds + i0 : nullptr, dout.rounds, (size_t)(i1 - i0) * 8},
+            {out->decision_rounds ? out->decision_rounds + i0 : nullptr, dout.decision_rounds, (size_t)(i1 - i0) * 8},
+            {out->evictions ? out->evictions + i0 : nullptr, dout.evictions, (size_t)(i1 - i0) * 8},
+            {out->makespan ? out->makespan + i0 : nullptr, dout.makespan, (size_t)(i1 - i0) * 4},
+            {out->peak_mem ? out->peak_mem + i0 : nullptr, dout.peak_mem, (size_t)(i1 - i0) * 4},
+            {out->status ? out->status + i0 : nullptr, dout.status, (size_t)(i1 - i0) * 4}};
+        for (auto &x : cp)
+            if (x.h && x.b) CUDA_TRY(c, cudaMemcpyAsync(x.h, x.d, x.b, cudaMemcpyDeviceToHost, c->s_out));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->s_out));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return SCHED_OK;
 }
@@ -579,6 +657,9 @@ int sched_finalize(sched_ctx *c)
             cudaEventDestroy(p.second);
         }
         for (auto e : c->free_events) cudaEventDestroy(e);
+        for (auto e : c->chunk_events) cudaEventDestroy(e);
+        if (c->s_in) cudaStreamDestroy(c->s_in);
+        if (c->s_out) cudaStreamDestroy(c->s_out);
     }
     delete c;
     return SCHED_OK;

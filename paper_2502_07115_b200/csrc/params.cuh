@@ -12,6 +12,7 @@ struct KParams {
     // batch
     long long n_inst;
     const long long *offset;
+    long long row_base;         // offset[k] - row_base = row of instance k's first request in req
     const int4 *req;            // {a, s, o, o~}
     const int *mem;
     unsigned long long id0;

@@ -333,6 +333,36 @@ def test_philox_known_answers_device(K, ctx):
     assert got[2] == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
 
 
+def _host_outputs(b):
+    outs = {"completion": np.empty(b.n_req, np.int32), "start": np.empty(b.n_req, np.int32)}
+    for k in ("tel", "rounds", "decision_rounds", "evictions"):
+        outs[k] = np.empty(b.n_inst, np.int64)
+    for k in ("makespan", "peak_mem", "status"):
+        outs[k] = np.empty(b.n_inst, np.int32)
+    return outs
+
+
+@pytest.mark.parametrize("pol", [0, 1, 2, 3, 4])
+def test_host_path_pipelined_chunks(K, ctx, oracle_mod, pol, monkeypatch):
+    """sched_run_instances_host cuts the batch into chunks (copy-in / kernel / copy-out on
+    three streams); with tiny chunks every policy and both kernels must still match."""
+    import paper_2502_07115_b200.kvsched as kv
+    monkeypatch.setenv("KVSCHED_HOST_CHUNK_ROWS", "997")
+    b = W.random_small(1500, 60 + pol, n_max=40, M_lo=6, M_hi=120, a_max=40)
+    if pol == 4:
+        b = W.with_prediction_noise(b, 0.3, seed=1)
+    kw = dict(alpha=(1, 10), beta_thresh=W.beta_threshold(0.3), seed=4) if pol >= 2 else {}
+    o = oracle_run(oracle_mod, b, pol, gid0=5, **kw)
+    outs = _host_outputs(b)
+    ctx.run_host(b.offset, b.req, b.mem, kv.Policy(KIND[pol], kw.get("alpha", (0, 1)), kw.get("beta_thresh", 0),
+                                                   kw.get("seed", 0)), outs, id0=5, hints=K.hints_of(b))
+    assert_parity(o, outs, b, "host chunks")
+    outs0 = _host_outputs(b)        # hints measured on the host
+    ctx.run_host(b.offset, b.req, b.mem, kv.Policy(KIND[pol], kw.get("alpha", (0, 1)), kw.get("beta_thresh", 0),
+                                                   kw.get("seed", 0)), outs0, id0=5)
+    assert_parity(o, outs0, b, "host chunks, measured hints")
+
+
 def test_host_path(K, ctx, oracle_mod):
     """sched_run_instances_host (host buffers, copies inside the call) gives the same bytes."""
     import paper_2502_07115_b200.kvsched as kv
