@@ -39,7 +39,7 @@
 #include "params.cuh"
 
 #ifndef KV_SMALL_MIN_BLOCKS
-#define KV_SMALL_MIN_BLOCKS 8
+#define KV_SMALL_MIN_BLOCKS 9
 #endif
 
 namespace kv {
@@ -66,6 +66,7 @@ __host__ __device__ inline int small_warp_bytes(int NP)
 // ---------------------------------------------------------------------------------------
 struct RegQueue {
     uint32_t word;
+    uint32_t hw;         // warp-uniform copy of the word holding the head (after first())
     uint32_t *stage;     // [32] shared staging words for inserts
 
     __device__ __forceinline__ void init(uint32_t *st, uint32_t *, int)
@@ -86,16 +87,23 @@ struct RegQueue {
         stage[lane_id()] = 0u;
         __syncwarp();
     }
-    __device__ __forceinline__ int first() const
+    // re-read the head's word after inserts (the head is the smallest rank, h != KV_INF)
+    __device__ __forceinline__ void refresh(int h) { hw = __shfl_sync(KV_FULL, word, h >> 5); }
+    __device__ __forceinline__ int first()
     {
         const uint32_t b = __ballot_sync(KV_FULL, word != 0u);
         if (b == 0u) return KV_INF;
         const int l0 = __ffs(b) - 1;
-        return (l0 << 5) + __ffs(__shfl_sync(KV_FULL, word, l0)) - 1;
+        hw = __shfl_sync(KV_FULL, word, l0);
+        return (l0 << 5) + __ffs(hw) - 1;
     }
+    // remove the head h (the smallest rank); the next head is usually in the same word
     __device__ __forceinline__ int pop(int h)
     {
-        if (lane_id() == (h >> 5)) word &= ~(1u << (h & 31));
+        const uint32_t bit = 1u << (h & 31);
+        if (lane_id() == (h >> 5)) word &= ~bit;
+        hw &= ~bit;
+        if (hw != 0u) return (h & ~31) + __ffs(hw) - 1;
         return first();
     }
 };
@@ -116,7 +124,8 @@ struct SmemQueue {
         if (take) q_insert(q, r);
     }
     __device__ __forceinline__ void flush() { __syncwarp(); }
-    __device__ __forceinline__ int first() const { return q_first(q); }
+    __device__ __forceinline__ void refresh(int) {}
+    __device__ __forceinline__ int first() { return q_first(q); }
     __device__ __forceinline__ int pop(int h) { return q_pop_head(q, h); }
 };
 
@@ -163,11 +172,15 @@ __device__ __forceinline__ int prof_max(int P0, int P1, int d)
 // and the answer is its first zero bit.  Offsets 0..31 are resolved first (one 32-bit
 // reduction); 32..63 only when all of those are blocked.  Prof is zero beyond tau = 63
 // (o~ <= 63), so the head fits by D = 64 at the latest.
+// bits [lo, hi] of a 32-bit word, relative to `base`, clipped to [0, 31]: 2^(hi+1) - 2^lo
+// with clamped funnel shifts (2^32 -> 0); empty when hi < lo
+__device__ __forceinline__ unsigned pow2c(int k) { return __funnelshift_lc(0u, 1u, (unsigned)k); }
+
 __device__ __forceinline__ unsigned interval_bits(int lo, int hi, int base)
 {
     lo = max(lo - base, 0);
-    hi = min(hi - base, 31);
-    return hi >= lo ? (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo) : 0u;
+    const int e = min(max(hi + 1 - base, lo), 32);
+    return pow2c(e) - pow2c(lo);
 }
 
 __device__ __forceinline__ int first_fit_offset(int P0, int P1, int s, int w, int M)
@@ -184,6 +197,183 @@ __device__ __forceinline__ int first_fit_offset(int P0, int P1, int s, int w, in
 }
 
 // ---------------------------------------------------------------------------------------
+// The round loop and the outputs of one instance; SLOW = some request has o~ > o (early
+// completions, MC-SF only), specialised so the o~ = o hot path carries none of it.
+template <int POL, bool MULTI, class Queue, bool SLOW>
+__device__ __forceinline__ void small_run(const KParams &P, long long inst, const SmallSmem &S, long long off,
+                                          int n, int M, long long suma, long long sumo)
+{
+    const int lane = lane_id();
+    InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
+    constexpr bool slow = SLOW;
+    Queue Q;
+    Q.init(S.sm, S.bm, (next_pow2(max(n, 32)) + 31) >> 5);
+
+    const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(S.arr[n - 1], sumo);
+    const int cap = (int)min(cap64, 0x7ffffffell);
+
+    // ---- round loop --------------------------------------------------------------------
+    int t = S.arr[0];
+    int next = 0, a_next = S.arr[0];
+    int h = KV_INF;                  // queue head (rank), KV_INF = R empty
+    uint32_t hkey = 0u;
+    bool hstale = false;
+    bool head_fits = false;          // the head's first-fit round was computed and reached
+    int P0 = 0, P1 = 0;              // Prof(t+lane+1), Prof(t+lane+33)
+    int rounds = 0, drounds = 0;
+    int maxc = -1, peak = 0, status = ST_OK;
+    // early-completion records (slow mode): one lane per in-flight request with o~ > o
+    int rc = KV_INF, rs = 0, rp = 0, rw = 0;
+
+    for (;;) {
+        if (h == KV_INF) {
+            if (!slow) {
+                if (a_next == KV_INF) {                       // drain: S only, no arrivals
+                    const int E = min(maxc, cap + 1);
+                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
+                    if (maxc > t) rounds += maxc - t;
+                    if (maxc >= cap + 1) status = ST_LIVELOCK;
+                    break;
+                }
+                const int tn = a_next;
+                if (tn > t) {                                 // skip rounds t..tn-1
+                    const int E = min(tn, cap + 1);
+                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
+                    rounds += max(0, min(tn, maxc) - t);
+                    if (tn > cap) { status = ST_LIVELOCK; break; }
+                    prof_shift(P0, P1, tn - t);
+                    t = tn;
+                }
+            } else if (maxc < t) {                            // S empty: idle jump
+                if (a_next == KV_INF) break;
+                t = max(t, a_next);
+            }
+        }
+        if (t > cap) { status = ST_LIVELOCK; break; }
+
+        // arrivals a_i <= t join R^(t) (P:91)
+        if (a_next <= t) {
+            do {
+                const int k = next + lane;
+                const int ak = k < n ? S.arr[k] : KV_INF;
+                const bool take = ak <= t;
+                const int cnt = __popc(__ballot_sync(KV_FULL, take));
+                const int rk = take ? ((POL == POL_MCSF) ? (int)S.arank[k] : k) : KV_INF;
+                Q.insert(take, rk);
+                const int mn = warp_min_i32(rk);
+                if (mn < h) { h = mn; hstale = true; head_fits = false; }
+                next += cnt;
+                a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? S.arr[next] : KV_INF);
+            } while (a_next <= t);
+            Q.flush();
+            Q.refresh(h);
+        }
+
+        // early completions (o~ > o): drop the unused projected tail (slow mode only)
+        if (slow) {
+            uint32_t m = __ballot_sync(KV_FULL, rc == t);
+            while (m) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                const int s_ = __shfl_sync(KV_FULL, rs, l), p_ = __shfl_sync(KV_FULL, rp, l);
+                const int e_ = __shfl_sync(KV_FULL, rw, l) + p_ - t;     // tau in [1, e_]
+                if (lane + 1 <= e_) P0 -= s_ + t + lane + 1 - p_;
+                if (lane + 33 <= e_) P1 -= s_ + t + lane + 33 - p_;
+                if (lane == l) rc = KV_INF;
+            }
+            if (h == KV_INF) {                 // R empty, S non-empty: one plain round
+                if (maxc > t) ++rounds;
+                peak = max(peak, __shfl_sync(KV_FULL, P0, 0));
+                prof_shift1(P0, P1);
+                ++t;
+                continue;
+            }
+        }
+
+        // decision round t with R non-empty (Alg. 1 / Alg. 2): candidates in rank order,
+        // break at the first failure.
+        if (hstale) { hkey = S.keys[h]; hstale = false; }
+        int jump = 1;
+        for (;;) {
+            const int w = (POL == POL_MCSF) ? (int)(hkey >> 26) : (int)(hkey & 63u);
+            const int s = (int)((hkey >> 6) & 63u), o = (int)(hkey & 63u);
+            if (MULTI) {
+                if (!head_fits) {
+                    const int d = first_fit_offset(P0, P1, s, w, M);
+                    if (d > 0) { jump = d; break; }                      // Eq. 5 violated now
+                }
+                head_fits = false;
+            } else {
+                const int tau0 = lane + 1, tau1 = lane + 33;
+                const bool v = (tau0 <= w && P0 + s + tau0 > M) || (tau1 <= w && P1 + s + tau1 > M);
+                if (__any_sync(KV_FULL, v)) break;                      // Eq. 5 violated
+            }
+            if (lane + 1 <= w) P0 += s + lane + 1;                       // ramp s + tau (Eq. 3)
+            if (lane + 33 <= w) P1 += s + lane + 33;
+            if (lane == 0) S.pst[(hkey >> 12) & 0x3fffu] = t;            // p_i = t
+            maxc = max(maxc, t + o);                                     // c_i = p_i + o_i
+            if (SLOW && w > o) {                                          // early completion
+                const uint32_t fr = __ballot_sync(KV_FULL, rc == KV_INF);
+                if (lane == __ffs(fr) - 1) { rc = t + o; rs = s; rp = t; rw = w; }
+            }
+            h = Q.pop(h);
+            if (h == KV_INF) break;
+            hkey = S.keys[h];
+        }
+        if (MULTI && jump > 1) {
+            int T = t + min(jump, cap + 1 - t);
+            if (slow) T = min(T, warp_min_i32(rc));
+            // an arrival before T ends the jump only if it becomes the new head, i.e. its
+            // key (o~, idx) precedes the blocked head's; in arrival order (MC-Benchmark) a
+            // newcomer never does.  Other arrivals join R at the landing round (no decision
+            // is taken in between, so when exactly they join does not matter).
+            if (POL == POL_MCSF) {
+                for (int k = next; a_next < T && k < n; k += 32) {
+                    const int kk = k + lane;
+                    const int ak = kk < n ? S.arr[kk] : KV_INF;
+                    const bool before = ak < T;
+                    const uint32_t m = __ballot_sync(KV_FULL, before && (int)S.arank[min(kk, n - 1)] < h);
+                    if (m) { T = __shfl_sync(KV_FULL, ak, __ffs(m) - 1); break; }
+                    if (!__all_sync(KV_FULL, before)) break;
+                }
+            }
+            head_fits = T == t + jump;        // landing where the unchanged head fits
+            jump = T - t;
+        }
+        // rounds t .. t+jump-1: decision rounds (R non-empty), batch memory Prof(t+1..t+jump)
+        drounds += jump;
+        rounds += jump;
+        if (jump == 1) {
+            peak = max(peak, __shfl_sync(KV_FULL, P0, 0));               // Mem(t+1)
+            prof_shift1(P0, P1);
+        } else {
+            peak = max(peak, prof_max(P0, P1, jump));
+            prof_shift(P0, P1, jump);
+        }
+        t += jump;
+    }
+
+    // ---- outputs: coalesced completion / start, TEL (P:95) ------------------------------
+    __syncwarp();
+    long long sumc = 0;
+    for (int k = lane; k < n; k += 32) {
+        const int p = S.pst[k];
+        const uint32_t key = (POL == POL_MCSF) ? S.kidx[k] : S.keys[k];
+        const int c = p < 0 ? -1 : p + (int)(key & 63u);
+        sumc += c;
+        if (P.completion) P.completion[off + k] = c;
+        if (P.start) P.start[off + k] = p;
+    }
+    sumc = warp_sum_i64(sumc);
+    res.tel = sumc - suma;
+    res.rounds = rounds;
+    res.decision_rounds = drounds;
+    res.makespan = maxc;
+    res.peak = peak;
+    res.status = status;
+    write_result(P, inst, res);
+}
+
 template <int POL, bool MULTI, class Queue>
 __device__ void small_instance(const KParams &P, long long inst, const SmallSmem &S)
 {
@@ -276,171 +466,8 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
             __syncwarp();
         }
     }
-    Queue Q;
-    Q.init(S.sm, S.bm, (next_pow2(max(n, 32)) + 31) >> 5);
-
-    const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(S.arr[n - 1], sumo);
-    const int cap = (int)min(cap64, 0x7ffffffell);
-
-    // ---- round loop --------------------------------------------------------------------
-    int t = S.arr[0];
-    int next = 0, a_next = S.arr[0];
-    int h = KV_INF;                  // queue head (rank), KV_INF = R empty
-    uint32_t hkey = 0u;
-    bool hstale = false;
-    bool head_fits = false;          // the head's first-fit round was computed and reached
-    int P0 = 0, P1 = 0;              // Prof(t+lane+1), Prof(t+lane+33)
-    int rounds = 0, drounds = 0;
-    int maxc = -1, peak = 0, status = ST_OK;
-    // early-completion records (slow mode): one lane per in-flight request with o~ > o
-    int rc = KV_INF, rs = 0, rp = 0, rw = 0;
-
-    for (;;) {
-        if (h == KV_INF) {
-            if (!slow) {
-                if (a_next == KV_INF) {                       // drain: S only, no arrivals
-                    const int E = min(maxc, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
-                    if (maxc > t) rounds += maxc - t;
-                    if (maxc >= cap + 1) status = ST_LIVELOCK;
-                    break;
-                }
-                const int tn = a_next;
-                if (tn > t) {                                 // skip rounds t..tn-1
-                    const int E = min(tn, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
-                    rounds += max(0, min(tn, maxc) - t);
-                    if (tn > cap) { status = ST_LIVELOCK; break; }
-                    prof_shift(P0, P1, tn - t);
-                    t = tn;
-                }
-            } else if (maxc < t) {                            // S empty: idle jump
-                if (a_next == KV_INF) break;
-                t = max(t, a_next);
-            }
-        }
-        if (t > cap) { status = ST_LIVELOCK; break; }
-
-        // arrivals a_i <= t join R^(t) (P:91)
-        if (a_next <= t) {
-            do {
-                const int k = next + lane;
-                const int ak = k < n ? S.arr[k] : KV_INF;
-                const bool take = ak <= t;
-                const int cnt = __popc(__ballot_sync(KV_FULL, take));
-                const int rk = take ? ((POL == POL_MCSF) ? (int)S.arank[k] : k) : KV_INF;
-                Q.insert(take, rk);
-                const int mn = warp_min_i32(rk);
-                if (mn < h) { h = mn; hstale = true; head_fits = false; }
-                next += cnt;
-                a_next = cnt < 32 ? __shfl_sync(KV_FULL, ak, cnt & 31) : (next < n ? S.arr[next] : KV_INF);
-            } while (a_next <= t);
-            Q.flush();
-        }
-
-        // early completions (o~ > o): drop the unused projected tail (slow mode only)
-        if (slow) {
-            uint32_t m = __ballot_sync(KV_FULL, rc == t);
-            while (m) {
-                const int l = __ffs(m) - 1;
-                m &= m - 1;
-                const int s_ = __shfl_sync(KV_FULL, rs, l), p_ = __shfl_sync(KV_FULL, rp, l);
-                const int e_ = __shfl_sync(KV_FULL, rw, l) + p_ - t;     // tau in [1, e_]
-                if (lane + 1 <= e_) P0 -= s_ + t + lane + 1 - p_;
-                if (lane + 33 <= e_) P1 -= s_ + t + lane + 33 - p_;
-                if (lane == l) rc = KV_INF;
-            }
-            if (h == KV_INF) {                 // R empty, S non-empty: one plain round
-                if (maxc > t) ++rounds;
-                peak = max(peak, __shfl_sync(KV_FULL, P0, 0));
-                prof_shift1(P0, P1);
-                ++t;
-                continue;
-            }
-        }
-
-        // decision round t with R non-empty (Alg. 1 / Alg. 2): candidates in rank order,
-        // break at the first failure.
-        if (hstale) { hkey = S.keys[h]; hstale = false; }
-        int jump = 1;
-        for (;;) {
-            const int w = (POL == POL_MCSF) ? (int)(hkey >> 26) : (int)(hkey & 63u);
-            const int s = (int)((hkey >> 6) & 63u), o = (int)(hkey & 63u);
-            if (MULTI) {
-                if (!head_fits) {
-                    const int d = first_fit_offset(P0, P1, s, w, M);
-                    if (d > 0) { jump = d; break; }                      // Eq. 5 violated now
-                }
-                head_fits = false;
-            } else {
-                const int tau0 = lane + 1, tau1 = lane + 33;
-                const bool v = (tau0 <= w && P0 + s + tau0 > M) || (tau1 <= w && P1 + s + tau1 > M);
-                if (__any_sync(KV_FULL, v)) break;                      // Eq. 5 violated
-            }
-            if (lane + 1 <= w) P0 += s + lane + 1;                       // ramp s + tau (Eq. 3)
-            if (lane + 33 <= w) P1 += s + lane + 33;
-            if (lane == 0) S.pst[(hkey >> 12) & 0x3fffu] = t;            // p_i = t
-            maxc = max(maxc, t + o);                                     // c_i = p_i + o_i
-            if (POL == POL_MCSF && w > o) {                               // early completion
-                const uint32_t fr = __ballot_sync(KV_FULL, rc == KV_INF);
-                if (lane == __ffs(fr) - 1) { rc = t + o; rs = s; rp = t; rw = w; }
-            }
-            h = Q.pop(h);
-            if (h == KV_INF) break;
-            hkey = S.keys[h];
-        }
-        if (MULTI && jump > 1) {
-            int T = t + min(jump, cap + 1 - t);
-            if (slow) T = min(T, warp_min_i32(rc));
-            // an arrival before T ends the jump only if it becomes the new head, i.e. its
-            // key (o~, idx) precedes the blocked head's; in arrival order (MC-Benchmark) a
-            // newcomer never does.  Other arrivals join R at the landing round (no decision
-            // is taken in between, so when exactly they join does not matter).
-            if (POL == POL_MCSF) {
-                for (int k = next; a_next < T && k < n; k += 32) {
-                    const int kk = k + lane;
-                    const int ak = kk < n ? S.arr[kk] : KV_INF;
-                    const bool before = ak < T;
-                    const uint32_t m = __ballot_sync(KV_FULL, before && (int)S.arank[min(kk, n - 1)] < h);
-                    if (m) { T = __shfl_sync(KV_FULL, ak, __ffs(m) - 1); break; }
-                    if (!__all_sync(KV_FULL, before)) break;
-                }
-            }
-            head_fits = T == t + jump;        // landing where the unchanged head fits
-            jump = T - t;
-        }
-        // rounds t .. t+jump-1: decision rounds (R non-empty), batch memory Prof(t+1..t+jump)
-        drounds += jump;
-        rounds += jump;
-        if (jump == 1) {
-            peak = max(peak, __shfl_sync(KV_FULL, P0, 0));               // Mem(t+1)
-            prof_shift1(P0, P1);
-        } else {
-            peak = max(peak, prof_max(P0, P1, jump));
-            prof_shift(P0, P1, jump);
-        }
-        t += jump;
-    }
-
-    // ---- outputs: coalesced completion / start, TEL (P:95) ------------------------------
-    __syncwarp();
-    long long sumc = 0;
-    for (int k = lane; k < n; k += 32) {
-        const int p = S.pst[k];
-        const uint32_t key = (POL == POL_MCSF) ? S.kidx[k] : S.keys[k];
-        const int c = p < 0 ? -1 : p + (int)(key & 63u);
-        sumc += c;
-        if (P.completion) P.completion[off + k] = c;
-        if (P.start) P.start[off + k] = p;
-    }
-    sumc = warp_sum_i64(sumc);
-    res.tel = sumc - suma;
-    res.rounds = rounds;
-    res.decision_rounds = drounds;
-    res.makespan = maxc;
-    res.peak = peak;
-    res.status = status;
-    write_result(P, inst, res);
+    if (POL == POL_MCSF && slow) small_run<POL, MULTI, Queue, true>(P, inst, S, off, n, M, suma, sumo);
+    else small_run<POL, MULTI, Queue, false>(P, inst, S, off, n, M, suma, sumo);
 }
 
 template <int POL, bool MULTI, bool QREG>
