@@ -384,7 +384,12 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     // rerun by a second launch whose ring covers every request plus the 32-round look-ahead.
     P.NP = next_pow2(max_req < 32 ? 32 : max_req);
     const int L_full = next_pow2(max_len + 33);
-    const int L_short = L_full < KV_RING_SHORT ? L_full : KV_RING_SHORT;
+    int ring_short = KV_RING_SHORT;                  // KVSCHED_RING_WINDOW: experiments only
+    if (const char *e = getenv("KVSCHED_RING_WINDOW")) {
+        const int v = atoi(e);
+        if (v >= 64 && (v & (v - 1)) == 0) ring_short = v;
+    }
+    const int L_short = L_full < ring_short ? L_full : ring_short;
     P.L = L_short;
     const bool prot = pol->policy == SCHED_MCSF_PROTECTED;
     auto wbytes = [&](int L) { return prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy); };
