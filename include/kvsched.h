@@ -157,6 +157,15 @@ int sched_run_instances_host(sched_ctx *ctx, const sched_instances *inst,
 int sched_latency(sched_ctx *ctx, const sched_instances *inst, const int32_t *completion,
                   int64_t *tel, int64_t *tel_total);
 
+/* Lower bound on the hindsight optimum (Eqs. 1-4) of instances whose requests all
+ * arrive at the same round: with vol_i = s_i o_i + o_i (o_i+1)/2, V_k the sum of the
+ * k smallest volumes and o_(k) the k-th smallest output length, the k-th completion is at
+ * least max(ceil(V_k / M), o_(k)) rounds after the arrival (volume argument of P:319), so
+ * lb[k] = sum_k max(ceil(V_k / M), o_(k)) <= OPT.  lb[k] = -1 if instance k's arrivals differ
+ * or it has more than 8192 requests; 0 if it is empty.  Device pointers; uses
+ * inst->max_requests as a hint (0 = measure).                                            */
+int sched_lb_sorted(sched_ctx *ctx, const sched_instances *inst, int64_t *lb);
+
 /* The counter-based RNG of the alpha-beta policy, exposed for known-answer tests:
  * out[4i..4i+3] = Philox4x32-10(counter ctr[4i..4i+3], key key[2i..2i+1]) (Salmon et al.,
  * SC'11) for i < n.  Device pointers.                                                    */

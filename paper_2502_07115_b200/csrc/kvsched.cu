@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/kvsched.h"
+#include "kernel_lb.cuh"
 #include "kernel_prot.cuh"
 #include "kernel_ring.cuh"
 #include "kernel_small.cuh"
@@ -591,6 +592,41 @@ int sched_latency(sched_ctx *c, const sched_instances *inst, const int32_t *comp
                                                   reinterpret_cast<const int4 *>(inst->req), completion,
                                                   reinterpret_cast<long long *>(tel),
                                                   reinterpret_cast<unsigned long long *>(tel_total));
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
+int sched_lb_sorted(sched_ctx *c, const sched_instances *inst, int64_t *lb)
+{
+    int rc = check_common(c, inst);
+    if (rc) return rc;
+    if (!lb) return fail(c, SCHED_E_ARG, "lb is NULL");
+    if (inst->n_instances == 0) return SCHED_OK;
+    DeviceGuard g(c->device);
+    int max_n = inst->max_requests;
+    if (max_n == 0) {
+        CUDA_TRY(c, cudaMemsetAsync(c->bounds.p, 0, 16, c->stream));
+        long long blocks = (inst->n_instances + 255) / 256;
+        if (blocks > 4 * (long long)c->num_sms) blocks = 4 * (long long)c->num_sms;
+        k_bounds<<<(int)blocks, 256, 0, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
+                                                     reinterpret_cast<const int4 *>(inst->req), inst->mem_limit,
+                                                     (int *)c->bounds.p);
+        CUDA_TRY(c, cudaGetLastError());
+        c->launches++;
+        int hb[4];
+        CUDA_TRY(c, cudaMemcpyAsync(hb, c->bounds.p, 16, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        max_n = hb[0];
+    }
+    if (max_n > 8192) max_n = 8192;                 // larger instances report -1
+    if (max_n < 2) max_n = 2;
+    const int smem = 2 * next_pow2(max_n) * 8;
+    CUDA_TRY(c, cudaFuncSetAttribute(k_lb_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    long long blocks = inst->n_instances < 8LL * c->num_sms ? inst->n_instances : 8LL * c->num_sms;
+    k_lb_sorted<<<(int)blocks, 512, smem, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
+                                                        reinterpret_cast<const int4 *>(inst->req), inst->mem_limit, max_n,
+                                                        reinterpret_cast<long long *>(lb));
     CUDA_TRY(c, cudaGetLastError());
     c->launches++;
     return SCHED_OK;

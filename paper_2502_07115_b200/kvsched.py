@@ -24,7 +24,8 @@ ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED
 
 # every symbol include/kvsched.h declares
 EXPORTS = ("sched_abi_version", "sched_init", "sched_set_stream", "sched_run_instances",
-           "sched_run_instances_host", "sched_latency", "sched_philox4x32_10", "sched_set_timing",
+           "sched_run_instances_host", "sched_latency", "sched_lb_sorted", "sched_philox4x32_10",
+           "sched_set_timing",
            "sched_get_stats", "sched_reset_stats", "sched_last_kernel", "sched_finalize",
            "sched_last_error")
 
@@ -74,6 +75,7 @@ def load() -> ctypes.CDLL:
                           ctypes.POINTER(SchedOutputs)]
         L.sched_latency.argtypes = [P, ctypes.POINTER(SchedInstances), P, P, P]
         L.sched_philox4x32_10.argtypes = [P, i64, P, P, P]
+        L.sched_lb_sorted.argtypes = [P, ctypes.POINTER(SchedInstances), P]
         L.sched_set_timing.argtypes = [P, ctypes.c_int]
         L.sched_get_stats.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(i64)]
@@ -176,6 +178,11 @@ class Context:
         si = SchedInstances(n, _ptr(offset), _ptr(req), None, 0, 0, 0, 0, 0)
         self._check(self._lib.sched_latency(self._h, ctypes.byref(si), _ptr(completion), _ptr(tel),
                                             _ptr(tel_total)), "sched_latency")
+
+    def lb_sorted(self, offset, req, mem, lb, hints=(0, 0, 0)) -> None:
+        """sched_lb_sorted: lb[k] = volume lower bound on OPT of simultaneous-arrival instances."""
+        si = self.instances(offset, req, mem, 0, hints)
+        self._check(self._lib.sched_lb_sorted(self._h, ctypes.byref(si), _ptr(lb)), "sched_lb_sorted")
 
     def philox(self, ctr, key, out) -> None:
         n = int(ctr.shape[0])

@@ -319,6 +319,30 @@ def test_latency_kernel(K, ctx, oracle_mod):
     assert tel[k].item() == -1
 
 
+def test_lb_sorted_kernel(K, ctx, oracle_mod):
+    """NEXT-2 (GPU part): the all-at-0 volume bound, bit-exact against the oracle's."""
+    import torch
+    batches = [W.c1(3000, 70, "a"), W.am1(64, 71), W.am1_paper(300, 72), W.am1(4, 73, n=5000, M=50),
+               W.from_instances([([], 9), ([[3, 1, 2, 2], [3, 2, 1, 1]], 9), ([[0, 1, 2, 2], [1, 1, 2, 2]], 9)])]
+    for b in batches:
+        dev = torch.device("cuda", 0)
+        off, req, mem = K.to_device(b, dev)
+        lb = torch.empty(b.n_inst, dtype=torch.int64, device=dev)
+        for hints in (K.hints_of(b), (0, 0, 0)):
+            ctx.lb_sorted(off, req, mem, lb, hints=hints)
+            torch.cuda.synchronize()
+            got = lb.cpu().numpy()
+            for k in range(b.n_inst):
+                r, M = b.instance(k)
+                if len(r) == 0:
+                    want = 0
+                elif (r[:, 0] != r[0, 0]).any():
+                    want = -1
+                else:
+                    want = oracle_mod.lb_sorted(r, M)
+                assert got[k] == want, (b.name, k, got[k], want)
+
+
 def test_philox_known_answers_device(K, ctx):
     import torch
     ctr = torch.tensor([[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]],
