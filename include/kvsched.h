@@ -72,12 +72,16 @@ enum {
     SCHED_INST_INVALID = 1,    /* data error: a not sorted, a < 0, s/o/o~ < 1; MC-SF: s+o~ > M
                                   or o~ < o; other policies: s+o > M (DESIGN Q8)          */
     SCHED_INST_LIVELOCK = 2,   /* round cap passed, or alpha head-of-line blocked for ever   */
-    SCHED_INST_UNSUPPORTED = 3 /* instance exceeds the caller's size hints / kernel limits  */
+    SCHED_INST_UNSUPPORTED = 3 /* instance exceeds the caller's size hints / kernel limits
+                                  (also: more than 32 requests longer than the 2048-round
+                                  ring window in flight at once when the full-length ring of
+                                  the rerun does not fit shared memory)                    */
 };
 
 /* Limits of this build (sched_run_instances returns SCHED_E_ARG beyond them). */
 #define SCHED_MAX_REQUESTS_PER_INSTANCE 32768
-#define SCHED_MAX_LEN 32767     /* max over requests of max(o, o~), also bounds M - 1 use */
+#define SCHED_MAX_LEN 32735     /* max over requests of max(o, o~): a 2^15-slot ring covers
+                                   a request's window plus the 32-round look-ahead          */
 
 /* sched_policy.flags.  SCHED_FLAG_PER_ROUND makes the MC kernels evaluate Eq. 5 for one
  * round per loop iteration instead of resolving a blocked queue head over up to 64

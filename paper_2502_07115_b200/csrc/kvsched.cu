@@ -160,6 +160,21 @@ __global__ void __launch_bounds__(128) k_latency(long long n_inst, const long lo
     }
 }
 
+// Instances handed to a full-ring rerun that cannot run: status UNSUPPORTED, no schedule.
+__global__ void k_mark_unsupported(const KParams P, const long long *list, const unsigned long long *count)
+{
+    const long long n = (long long)*count;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (long long w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += warps) {
+        const long long inst = list[w];
+        const long long off = P.offset[inst] - P.row_base;
+        const int m = (int)(P.offset[inst + 1] - P.offset[inst]);
+        fill_unscheduled(P, off, m);
+        InstResult res{0, 0, 0, 0, 0, 0, ST_UNSUPPORTED};
+        write_result(P, inst, res);
+    }
+}
+
 __global__ void k_philox(long long n, const uint4 *ctr, const uint2 *key, uint4 *out)
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -395,9 +410,9 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     const bool prot = pol->policy == SCHED_MCSF_PROTECTED;
     auto wbytes = [&](int L) { return prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy); };
     P.warp_bytes = wbytes(P.L);
-    if ((size_t)wbytes(L_full) > c->max_smem_optin)
+    if ((size_t)P.warp_bytes > c->max_smem_optin)
         return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
-                    wbytes(L_full), L_full, P.NP);
+                    P.warp_bytes, P.L, P.NP);
     if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
     P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
     P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
@@ -435,7 +450,13 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         }
     };
     if ((rc = launch_ring(P))) return rc;
-    if (L_short < L_full) {
+    if (L_short < L_full && (size_t)wbytes(L_full) > c->max_smem_optin) {
+        // no room for the full ring: the (rare) instances that overflowed the long list
+        // are reported UNSUPPORTED
+        k_mark_unsupported<<<64, 128, 0, c->stream>>>(P, P.retry_list, P.retry_count);
+        CUDA_TRY(c, cudaGetLastError());
+        c->launches++;
+    } else if (L_short < L_full) {
         KParams Q = P;
         Q.L = L_full;
         Q.warp_bytes = wbytes(L_full);

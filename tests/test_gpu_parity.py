@@ -319,6 +319,47 @@ def test_latency_kernel(K, ctx, oracle_mod):
     assert tel[k].item() == -1
 
 
+@pytest.mark.parametrize("pol", [0, 1, 2])
+def test_maximum_sizes(K, ctx, oracle_mod, pol):
+    """Instances at the build limits: 32768 requests (ring kernel), 16384 requests with
+    M <= 64 (fused kernel, shared-memory queue), a request of length 32735 (SCHED_MAX_LEN)."""
+    g = np.random.default_rng(80 + pol)
+    n = 32768
+    a = np.sort(g.integers(0, 20000, n))
+    s_ = g.integers(1, 40, n)
+    o = g.integers(1, 300, n)
+    big = np.stack([a, s_, o, o], 1)
+    n2 = 16384
+    a2 = np.sort(g.integers(0, 3000, n2))
+    s2 = g.integers(1, 6, n2)
+    o2 = g.integers(1, 40, n2)
+    small = np.stack([a2, s2, o2, o2], 1)
+    longest = np.array([[0, 1, 32735, 32735], [5, 10, 100, 100], [7, 3, 20000, 20000]])
+    b = W.from_instances([(big, 2000)])
+    c = W.from_instances([(small, 48)])
+    d = W.from_instances([(longest, 40000)])
+    kw = dict(alpha=(1, 10)) if pol >= 2 else {}
+    check(K, ctx, oracle_mod, b, pol, "n=32768", **kw)
+    if pol < 2:
+        check(K, ctx, oracle_mod, c, pol, "n=16384 small kernel", **kw)
+    check(K, ctx, oracle_mod, d, pol, "length 32767", **kw)
+
+
+def test_long_list_overflow_without_room_is_unsupported(K, ctx, oracle_mod):
+    """k_prot keeps three rings per warp; a full-length rerun ring of 2^15 slots does not fit
+    shared memory, so an instance with more than 32 long requests in flight is reported
+    UNSUPPORTED (and only that one), never a wrong schedule."""
+    many = ([[0, 1, 20000, 20000]] * 40, 2_000_000)
+    fine = ([[0, 2, 30, 30], [3, 1, 20000, 20000]], 100_000)
+    b = W.from_instances([fine, many, fine])
+    g = gpu_run(K, ctx, b, 4, alpha=(1, 10))
+    assert list(g["status"]) == [0, 3, 0]
+    o = oracle_run(oracle_mod, b.subset([0, 2]), 4, alpha=(1, 10))
+    assert list(o["tel"]) == [g["tel"][0], g["tel"][2]]
+    lo, hi = int(b.offset[1]), int(b.offset[2])
+    assert (g["completion"][lo:hi] == -1).all()
+
+
 def test_lb_sorted_kernel(K, ctx, oracle_mod):
     """NEXT-2 (GPU part): the all-at-0 volume bound, bit-exact against the oracle's."""
     import torch

@@ -270,13 +270,13 @@ def random_small(n_inst: int, seed: int, n_max: int = 40, M_lo: int = 4, M_hi: i
 def with_prediction_noise(b: Batch, eps: float, seed: int = 7) -> Batch:
     """Replace o~ by a noisy prediction o^ ~ U((1-eps)o, (1+eps)o), rounded to
     an integer >= 1 on the host (DESIGN Q26): o^ = max(1, floor(o (1 + eps (2u - 1)) + 0.5)).
-    Predictions may under- or over-shoot o; they are capped at 32767 (the build's length limit)."""
+    Predictions may under- or over-shoot o; they are capped at 32735 (the build's length limit)."""
     g = _rng([13, seed, int(round(eps * 1000))])
     u = g.random(b.n_req)
     o = b.req[:, 2].astype(np.float64)
     pred = np.maximum(1, np.floor(o * (1.0 + eps * (2.0 * u - 1.0)) + 0.5)).astype(np.int64)
     req = b.req.copy()
-    req[:, 3] = np.minimum(pred, 32767)
+    req[:, 3] = np.minimum(pred, 32735)
     meta = dict(b.meta)
     meta["prediction_noise_eps"] = eps
     return Batch(b.offset.copy(), req, b.mem.copy(), b.name + f"+noise{eps}", meta)
