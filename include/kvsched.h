@@ -170,6 +170,36 @@ int sched_latency(sched_ctx *ctx, const sched_instances *inst, const int32_t *co
  * inst->max_requests as a hint (0 = measure).                                            */
 int sched_lb_sorted(sched_ctx *ctx, const sched_instances *inst, int64_t *lb);
 
+/* On-device generation of Arrival-Model-2 instances on a lambda x M sweep grid
+ * (configuration C5), from an integer counter-based specification; the bytes equal those of
+ * the host reference workloads.am2_counter.  Instance k (global id g = instance_id0 + k):
+ *   cell = g mod (n_lambda n_m); lambda index = cell / n_m; M = m_values[cell mod n_m];
+ *   u(stream, j) = Philox4x32-10(counter (lo32 g, hi32 g, stream, j), key (lo32 seed, hi32 seed));
+ *   mulhi(u, r) = (u r) >> 32;
+ *   T = T_lo + mulhi(u(0,0)[0], T_hi - T_lo + 1);
+ *   arrivals at round r = 1..T: the smallest c with u(1,r)[0] < poisson_cdf[lambda][c];
+ *   request i in arrival order: s = s_lo + mulhi(u(2,i)[0], s_hi - s_lo + 1),
+ *   o = 1 + mulhi(u(2,i)[1], M - s), o~ = o.
+ * poisson_cdf[l][c] = floor(P(Poisson(lambda_l) <= c) 2^32), c = 0..31, the last = 2^32.
+ * Requires 0 <= T_lo <= T_hi <= 1024, 1 <= s_lo <= s_hi < every m_value.                */
+typedef struct {
+    int64_t n_instances;
+    int64_t instance_id0;
+    uint64_t seed;
+    int32_t n_lambda, n_m;
+    const uint64_t *poisson_cdf;  /* device [n_lambda][32]                                  */
+    const int32_t *m_values;      /* device [n_m]                                           */
+    int32_t T_lo, T_hi, s_lo, s_hi;
+} sched_gen_am2;
+
+/* req_offset[0..n] (device) <- CSR offsets of the generated batch (count + device scan).   */
+int sched_gen_am2_count(sched_ctx *ctx, const sched_gen_am2 *spec, int64_t *req_offset);
+
+/* Fill req [req_offset[n]][4] {a, s, o, o~} and mem_limit [n] (device) for the offsets that
+ * sched_gen_am2_count produced.                                                           */
+int sched_gen_am2_fill(sched_ctx *ctx, const sched_gen_am2 *spec, const int64_t *req_offset,
+                       int32_t *req, int32_t *mem_limit);
+
 /* The counter-based RNG of the alpha-beta policy, exposed for known-answer tests:
  * out[4i..4i+3] = Philox4x32-10(counter ctr[4i..4i+3], key key[2i..2i+1]) (Salmon et al.,
  * SC'11) for i < n.  Device pointers.                                                    */

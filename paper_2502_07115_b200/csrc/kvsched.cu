@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/kvsched.h"
+#include "kernel_gen.cuh"
 #include "kernel_lb.cuh"
 #include "kernel_prot.cuh"
 #include "kernel_ring.cuh"
@@ -42,7 +43,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry;
+    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -653,6 +654,69 @@ int sched_lb_sorted(sched_ctx *c, const sched_instances *inst, int64_t *lb)
     return SCHED_OK;
 }
 
+static int gen_params(sched_ctx *c, const sched_gen_am2 *sp, GenAm2 *G)
+{
+    if (!sp) return fail(c, SCHED_E_ARG, "spec is NULL");
+    if (sp->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
+    if (sp->n_lambda < 1 || sp->n_m < 1 || !sp->poisson_cdf || !sp->m_values)
+        return fail(c, SCHED_E_ARG, "need n_lambda, n_m >= 1 and the tables");
+    if (sp->T_lo < 0 || sp->T_hi < sp->T_lo || sp->T_hi > 1024)
+        return fail(c, SCHED_E_ARG, "need 0 <= T_lo <= T_hi <= 1024");
+    if (sp->s_lo < 1 || sp->s_hi < sp->s_lo) return fail(c, SCHED_E_ARG, "need 1 <= s_lo <= s_hi");
+    *G = GenAm2{sp->n_instances, sp->instance_id0, sp->seed, sp->n_lambda, sp->n_m,
+                reinterpret_cast<const unsigned long long *>(sp->poisson_cdf), sp->m_values,
+                sp->T_lo, sp->T_hi, sp->s_lo, sp->s_hi};
+    return SCHED_OK;
+}
+
+int sched_gen_am2_count(sched_ctx *c, const sched_gen_am2 *spec, int64_t *req_offset)
+{
+    if (!c) return SCHED_E_STATE;
+    GenAm2 G;
+    int rc = gen_params(c, spec, &G);
+    if (rc) return rc;
+    if (!req_offset) return fail(c, SCHED_E_ARG, "req_offset is NULL");
+    DeviceGuard g(c->device);
+    long long *x = reinterpret_cast<long long *>(req_offset);
+    if (G.n_inst == 0) {
+        CUDA_TRY(c, cudaMemsetAsync(x, 0, 8, c->stream));
+        return SCHED_OK;
+    }
+    long long blocks = (G.n_inst + 255) / 256;
+    if (blocks > 16LL * c->num_sms) blocks = 16LL * c->num_sms;
+    k_gen_am2_count<<<(int)blocks, 256, 0, c->stream>>>(G, x);
+    CUDA_TRY(c, cudaGetLastError());
+    const long long nb = (G.n_inst + kScanBlock - 1) / kScanBlock;
+    if ((rc = grow(c, c->scan, (size_t)nb * 8))) return rc;
+    long long *bs = reinterpret_cast<long long *>(c->scan.p);
+    k_scan_blocks<<<(int)nb, kScanBlock, 0, c->stream>>>(x, G.n_inst, bs);
+    k_scan_sums<<<1, kScanBlock, 0, c->stream>>>(bs, nb);
+    k_scan_fix<<<(int)nb, kScanBlock, 0, c->stream>>>(x, G.n_inst, bs);
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches += 4;
+    return SCHED_OK;
+}
+
+int sched_gen_am2_fill(sched_ctx *c, const sched_gen_am2 *spec, const int64_t *req_offset, int32_t *req,
+                       int32_t *mem_limit)
+{
+    if (!c) return SCHED_E_STATE;
+    GenAm2 G;
+    int rc = gen_params(c, spec, &G);
+    if (rc) return rc;
+    if (G.n_inst == 0) return SCHED_OK;
+    if (!req_offset || !req || !mem_limit) return fail(c, SCHED_E_ARG, "null output");
+    if (((uintptr_t)req) & 15u) return fail(c, SCHED_E_ARG, "req must be 16-byte aligned");
+    DeviceGuard g(c->device);
+    long long blocks = (G.n_inst + 3) / 4;
+    if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
+    k_gen_am2_fill<<<(int)blocks, 128, 0, c->stream>>>(G, reinterpret_cast<const long long *>(req_offset),
+                                                        reinterpret_cast<int4 *>(req), mem_limit);
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
 int sched_philox4x32_10(sched_ctx *c, int64_t n, const uint32_t *ctr, const uint32_t *key, uint32_t *out)
 {
     if (!c) return SCHED_E_STATE;
@@ -711,7 +775,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {

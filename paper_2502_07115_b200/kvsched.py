@@ -24,7 +24,8 @@ ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED
 
 # every symbol include/kvsched.h declares
 EXPORTS = ("sched_abi_version", "sched_init", "sched_set_stream", "sched_run_instances",
-           "sched_run_instances_host", "sched_latency", "sched_lb_sorted", "sched_philox4x32_10",
+           "sched_run_instances_host", "sched_latency", "sched_lb_sorted", "sched_gen_am2_count",
+           "sched_gen_am2_fill", "sched_philox4x32_10",
            "sched_set_timing",
            "sched_get_stats", "sched_reset_stats", "sched_last_kernel", "sched_finalize",
            "sched_last_error")
@@ -42,6 +43,12 @@ class SchedInstances(ctypes.Structure):
 class SchedPolicy(ctypes.Structure):
     _fields_ = [("policy", i32), ("alpha_num", i32), ("alpha_den", i32), ("flags", i32),
                 ("beta_thresh", u64), ("seed", u64), ("round_cap", i64)]
+
+
+class SchedGenAm2(ctypes.Structure):
+    _fields_ = [("n_instances", i64), ("instance_id0", i64), ("seed", u64), ("n_lambda", i32),
+                ("n_m", i32), ("poisson_cdf", P), ("m_values", P), ("T_lo", i32), ("T_hi", i32),
+                ("s_lo", i32), ("s_hi", i32)]
 
 
 class SchedOutputs(ctypes.Structure):
@@ -76,6 +83,8 @@ def load() -> ctypes.CDLL:
         L.sched_latency.argtypes = [P, ctypes.POINTER(SchedInstances), P, P, P]
         L.sched_philox4x32_10.argtypes = [P, i64, P, P, P]
         L.sched_lb_sorted.argtypes = [P, ctypes.POINTER(SchedInstances), P]
+        L.sched_gen_am2_count.argtypes = [P, ctypes.POINTER(SchedGenAm2), P]
+        L.sched_gen_am2_fill.argtypes = [P, ctypes.POINTER(SchedGenAm2), P, P, P]
         L.sched_set_timing.argtypes = [P, ctypes.c_int]
         L.sched_get_stats.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(i64)]
@@ -183,6 +192,25 @@ class Context:
         """sched_lb_sorted: lb[k] = volume lower bound on OPT of simultaneous-arrival instances."""
         si = self.instances(offset, req, mem, 0, hints)
         self._check(self._lib.sched_lb_sorted(self._h, ctypes.byref(si), _ptr(lb)), "sched_lb_sorted")
+
+    def gen_am2(self, n_inst: int, spec, id0: int = 0):
+        """NEXT-3: generate an AM2-grid batch on the device (sched_gen_am2_count + _fill).
+        `spec` is a workloads.Am2Spec; returns device tensors (offset, req, mem)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        cdf = torch.from_numpy(spec.tables().astype(np.uint64).view(np.int64)).to(dev)
+        ms = torch.tensor(list(spec.Ms), dtype=torch.int32, device=dev)
+        g = SchedGenAm2(int(n_inst), int(id0), int(spec.seed) & (2**64 - 1), len(spec.lambdas), len(spec.Ms),
+                        cdf.data_ptr(), ms.data_ptr(), int(spec.T_lo), int(spec.T_hi), int(spec.s_lo),
+                        int(spec.s_hi))
+        off = torch.empty(int(n_inst) + 1, dtype=torch.int64, device=dev)
+        self._check(self._lib.sched_gen_am2_count(self._h, ctypes.byref(g), off.data_ptr()), "sched_gen_am2_count")
+        n_req = int(off[-1].item())                      # one 8-byte read to size the rows
+        req = torch.empty((max(n_req, 1), 4), dtype=torch.int32, device=dev)
+        mem = torch.empty(max(int(n_inst), 1), dtype=torch.int32, device=dev)
+        self._check(self._lib.sched_gen_am2_fill(self._h, ctypes.byref(g), off.data_ptr(), req.data_ptr(),
+                                                 mem.data_ptr()), "sched_gen_am2_fill")
+        return off, req[:max(n_req, 1)], mem[:max(int(n_inst), 1)], n_req
 
     def philox(self, ctr, key, out) -> None:
         n = int(ctr.shape[0])

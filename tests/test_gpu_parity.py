@@ -360,6 +360,34 @@ def test_long_list_overflow_without_room_is_unsupported(K, ctx, oracle_mod):
     assert (g["completion"][lo:hi] == -1).all()
 
 
+@pytest.mark.parametrize("n_inst,id0,seed", [(1, 0, 1), (3000, 0, 12345), (4097, 2**33 + 5, 7), (100000, 10**6, 99)])
+def test_device_generation_matches_host_reference(K, ctx, oracle_mod, n_inst, id0, seed):
+    """NEXT-3: sched_gen_am2 writes exactly the bytes of workloads.am2_counter; the
+    generated batch then simulates to the oracle's schedules."""
+    spec = W.Am2Spec(seed=seed)
+    off, req, mem, n_req = ctx.gen_am2(n_inst, spec, id0=id0)
+    import torch
+    torch.cuda.synchronize()
+    h = W.am2_counter(n_inst, spec, id0=id0)
+    assert n_req == h.n_req
+    assert np.array_equal(off.cpu().numpy(), h.offset)
+    assert np.array_equal(req.cpu().numpy()[:n_req], h.req)
+    assert np.array_equal(mem.cpu().numpy()[:n_inst], h.mem)
+    if n_inst <= 4097:
+        check(K, ctx, oracle_mod, h, 0, "generated batch")
+
+
+def test_device_generation_edge_specs(K, ctx):
+    """T_lo = T_hi = 0 (every instance empty) and a single-cell grid with a large lambda."""
+    import torch
+    for spec in (W.Am2Spec(T_lo=0, T_hi=0, seed=3), W.Am2Spec(lambdas=(6.0,), Ms=(64,), T_lo=1, T_hi=1024, s_lo=2, s_hi=9, seed=4)):
+        off, req, mem, n_req = ctx.gen_am2(257, spec, id0=11)
+        torch.cuda.synchronize()
+        h = W.am2_counter(257, spec, id0=11)
+        assert np.array_equal(off.cpu().numpy(), h.offset)
+        assert np.array_equal(req.cpu().numpy()[:n_req], h.req[:n_req])
+
+
 def test_lb_sorted_kernel(K, ctx, oracle_mod):
     """NEXT-2 (GPU part): the all-at-0 volume bound, bit-exact against the oracle's."""
     import torch

@@ -49,3 +49,29 @@ def test_trace_moments():
     span = b.instance(0)[0][-1, 0]
     assert abs(span - 5000) < 400
     assert abs(math.sqrt(2 * math.log(40.62 / 11)) - 1.616) < 1e-3
+
+
+def test_counter_generator_spec():
+    """NEXT-3 host reference (workloads.am2_counter): deterministic, on the grid, ranges of
+    P:408 (T in [40, 60], arrivals on rounds 1..T, s in [1, 5], o in [1, M - s]), Poisson
+    counts with the right mean, Philox matching the published known-answer vector."""
+    c = W._philox_np(np.array([0x243F6A88], np.uint32), np.array([0x85A308D3], np.uint32),
+                     np.array([0x13198A2E], np.uint32), np.array([0x03707344], np.uint32),
+                     np.array([0xA4093822], np.uint32), np.array([0x299F31D0], np.uint32))
+    assert [int(x[0]) for x in c] == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+    t = W.poisson_cdf_table(1.0)
+    assert (np.diff(t.astype(np.int64)) >= 0).all() and t[-1] == 2 ** 32
+    assert abs(int(t[0]) / 2 ** 32 - math.exp(-1.0)) < 1e-9
+    spec = W.Am2Spec()
+    b = W.am2_counter(5000, spec, id0=123)
+    assert b.sha256() == W.am2_counter(5000, spec, id0=123).sha256()
+    _check_batch(b)
+    assert b.req[:, 0].min() >= 1 and b.req[:, 0].max() <= 60
+    assert b.req[:, 1].min() >= 1 and b.req[:, 1].max() <= 5
+    cells = (np.arange(123, 5123) % 25)
+    assert (b.mem == np.array(W.C5_MS)[cells % 5]).all()
+    lam = np.array(W.C5_LAMBDAS)[cells // 5]
+    assert abs(b.sizes().mean() / (lam * 50).mean() - 1) < 0.02
+    # shards of the global id range concatenate to the whole
+    x, y = W.am2_counter(2000, spec, id0=123), W.am2_counter(3000, spec, id0=2123)
+    assert np.array_equal(np.concatenate([x.req, y.req]), b.req)

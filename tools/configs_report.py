@@ -159,6 +159,31 @@ def main():
     report["C5"] = r
     print("C5", json.dumps(r), flush=True)
 
+    # NEXT-3: the C5 sweep generated on the device from the counter spec, then simulated
+    spec = W.Am2Spec(seed=5)
+    n = 200_000 if q else 1_000_000
+    off, req, mem, n_req = ctx.gen_am2(n, spec)          # warm-up (allocations)
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    off, req, mem, n_req = ctx.gen_am2(n, spec)
+    e1.record()
+    out = K.alloc_outputs(n, n_req, torch.device("cuda", 0))
+    hints = (int(torch.diff(off).max().item()), max(spec.Ms), max(spec.Ms) - spec.s_lo)
+    e1b = torch.cuda.Event(enable_timing=True)
+    e1b.record()
+    ctx.run(off, req, mem, K.Policy("mcsf"), out, hints=hints)
+    e2.record()
+    torch.cuda.synchronize()
+    rounds = int(out["rounds"][:n].clamp(min=0).sum().item())
+    hb = W.am2_counter(2000, spec)
+    r = {"instances": n, "requests": n_req, "generate_ms": e0.elapsed_time(e1), "simulate_ms": e1b.elapsed_time(e2),
+         "generated_instances_per_s": n / (e0.elapsed_time(e1) / 1e3),
+         "rounds_per_s_simulation": rounds / (e1b.elapsed_time(e2) / 1e3),
+         "bytes_match_host_reference_first_2000": bool(np.array_equal(req[:hb.n_req].cpu().numpy(), hb.req))}
+    report["C5 generated on device (NEXT-3)"] = r
+    print("C5gen", json.dumps(r), flush=True)
+
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     Path(a.out).write_text(json.dumps(report, indent=1))
     ctx.close()

@@ -280,3 +280,104 @@ def with_prediction_noise(b: Batch, eps: float, seed: int = 7) -> Batch:
     meta = dict(b.meta)
     meta["prediction_noise_eps"] = eps
     return Batch(b.offset.copy(), req, b.mem.copy(), b.name + f"+noise{eps}", meta)
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-3: the AM2-grid generator as an integer counter-based spec (host reference).
+# The CUDA path implements the same spec in sched_gen_am2_{count,fill}; both consume the same
+# Poisson inversion tables (computed here, passed as inputs) so no floating point is involved
+# in either generator.
+#
+#   instance g (global id), cell = g mod (|lambdas| |Ms|), lambda = lambdas[cell // |Ms|],
+#   M = Ms[cell % |Ms|];  u(stream, j) = Philox4x32-10(counter (lo32 g, hi32 g, stream, j),
+#   key (lo32 seed, hi32 seed));  mulhi(u, r) = (u * r) >> 32
+#   T     = T_lo + mulhi(u(0, 0).x, T_hi - T_lo + 1)
+#   count(r) for rounds r = 1..T: smallest c with u(1, r).x < cdf[lambda][c]  (c <= 31)
+#   requests i = 0.. in arrival order: w = u(2, i); s = s_lo + mulhi(w.x, s_hi - s_lo + 1);
+#   o = 1 + mulhi(w.y, M - s); o~ = o
+# ---------------------------------------------------------------------------------------
+GEN_AM2_VERSION = "am2-grid-v1"
+POISSON_TABLE_LEN = 32
+
+
+def _philox_np(c0, c1, c2, c3, k0, k1):
+    """Philox4x32-10 (Salmon et al., SC'11) on uint32 numpy arrays."""
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint32).copy() for x in (c0, c1, c2, c3))
+    k0 = np.asarray(k0, dtype=np.uint32).copy()
+    k1 = np.asarray(k1, dtype=np.uint32).copy()
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = c0.astype(np.uint64) * M0
+            p1 = c2.astype(np.uint64) * M1
+            hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), p0.astype(np.uint32)
+            hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), p1.astype(np.uint32)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0 = k0 + W0
+            k1 = k1 + W1
+    return c0, c1, c2, c3
+
+
+def _mulhi(u, r):
+    return ((np.asarray(u, dtype=np.uint64) * np.asarray(r, dtype=np.uint64)) >> np.uint64(32)).astype(np.int64)
+
+
+def poisson_cdf_table(lam: float) -> np.ndarray:
+    """uint64 thresholds floor(P(X <= c) 2^32), c = 0..31, last one forced to 2^32."""
+    p = math.exp(-lam)
+    acc, out = 0.0, []
+    for c in range(POISSON_TABLE_LEN):
+        acc += p
+        out.append(min(int(acc * 2.0 ** 32), 2 ** 32))
+        p *= lam / (c + 1)
+    out[-1] = 2 ** 32
+    return np.array(out, dtype=np.uint64)
+
+
+@dataclass
+class Am2Spec:
+    lambdas: tuple = C5_LAMBDAS
+    Ms: tuple = C5_MS
+    T_lo: int = 40
+    T_hi: int = 60
+    s_lo: int = 1
+    s_hi: int = 5
+    seed: int = 12345
+
+    def tables(self) -> np.ndarray:
+        return np.stack([poisson_cdf_table(l) for l in self.lambdas])
+
+
+def am2_counter(n_inst: int, spec: Am2Spec = Am2Spec(), id0: int = 0) -> Batch:
+    """Host reference of the counter-based AM2-grid generator (the spec above)."""
+    g = np.arange(id0, id0 + n_inst, dtype=np.uint64)
+    glo, ghi = (g & np.uint64(0xFFFFFFFF)).astype(np.uint32), (g >> np.uint64(32)).astype(np.uint32)
+    k0 = np.full(n_inst, spec.seed & 0xFFFFFFFF, dtype=np.uint32)
+    k1 = np.full(n_inst, (spec.seed >> 32) & 0xFFFFFFFF, dtype=np.uint32)
+    ncell = len(spec.lambdas) * len(spec.Ms)
+    cell = (g % np.uint64(ncell)).astype(np.int64)
+    li, mi = cell // len(spec.Ms), cell % len(spec.Ms)
+    M = np.asarray(spec.Ms, dtype=np.int64)[mi]
+    cdf = spec.tables()
+    z = np.zeros(n_inst, dtype=np.uint32)
+    T = spec.T_lo + _mulhi(_philox_np(glo, ghi, z, z, k0, k1)[0], spec.T_hi - spec.T_lo + 1)
+    counts = np.zeros((n_inst, spec.T_hi), dtype=np.int64)
+    for r in range(1, spec.T_hi + 1):
+        u = _philox_np(glo, ghi, np.full(n_inst, 1, np.uint32), np.full(n_inst, r, np.uint32), k0, k1)[0]
+        c = (u.astype(np.uint64)[:, None] >= cdf[li]).sum(axis=1)      # smallest c with u < cdf[c]
+        counts[:, r - 1] = np.where(r <= T, c, 0)
+    sizes = counts.sum(axis=1)
+    rounds = np.broadcast_to(np.arange(1, spec.T_hi + 1, dtype=np.int64), counts.shape)
+    a = np.repeat(rounds.ravel(), counts.ravel())
+    inst = np.repeat(np.arange(n_inst), sizes)
+    start = np.zeros(n_inst + 1, dtype=np.int64)
+    np.cumsum(sizes, out=start[1:])
+    i = np.arange(a.shape[0], dtype=np.int64) - start[inst]
+    gg = g[inst]
+    w = _philox_np((gg & np.uint64(0xFFFFFFFF)).astype(np.uint32), (gg >> np.uint64(32)).astype(np.uint32),
+                   np.full(a.shape[0], 2, np.uint32), i.astype(np.uint32), k0[inst], k1[inst])
+    s = spec.s_lo + _mulhi(w[0], spec.s_hi - spec.s_lo + 1)
+    o = 1 + _mulhi(w[1], np.maximum(M[inst] - s, 0))
+    b = _assemble(a, s, o, sizes, M, "C5-counter", dict(spec=GEN_AM2_VERSION, seed=spec.seed, id0=id0))
+    return b
