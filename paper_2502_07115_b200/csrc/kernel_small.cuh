@@ -155,13 +155,13 @@ __device__ __forceinline__ void prof_shift1(int &P0, int &P1)
     P1 = lane == 31 ? 0 : n1;
 }
 
-// max of Prof(t+tau) over tau in [1, d]
-__device__ __forceinline__ int prof_max(int P0, int P1, int d)
+// this lane's share of max Prof(t+tau) over tau in [1, d] (the warp maximum is taken once,
+// when the instance ends)
+__device__ __forceinline__ int prof_max_lane(int P0, int P1, int d)
 {
     const int lane = lane_id();
-    int v = (lane + 1 <= d) ? P0 : 0;
-    v = max(v, (lane + 33 <= d) ? P1 : 0);
-    return warp_max_i32(v);
+    const int v = (lane + 1 <= d) ? P0 : 0;
+    return max(v, (lane + 33 <= d) ? P1 : 0);
 }
 
 // First round offset D >= 0 at which a head candidate (s, w) satisfies Eq. 5 while the
@@ -220,8 +220,8 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
     bool hstale = false;
     bool head_fits = false;          // the head's first-fit round was computed and reached
     int P0 = 0, P1 = 0;              // Prof(t+lane+1), Prof(t+lane+33)
-    int rounds = 0, drounds = 0;
-    int maxc = -1, peak = 0, status = ST_OK;
+    int rounds = 0, drounds = 0;     // rounds: non-idle rounds that were not decision rounds
+    int maxc = -1, peak = 0, status = ST_OK;   // peak: per-lane partial maximum
     // early-completion records (slow mode): one lane per in-flight request with o~ > o
     int rc = KV_INF, rs = 0, rp = 0, rw = 0;
 
@@ -230,7 +230,7 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
             if (!slow) {
                 if (a_next == KV_INF) {                       // drain: S only, no arrivals
                     const int E = min(maxc, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
+                    if (E > t) peak = max(peak, prof_max_lane(P0, P1, min(E - t, 64)));
                     if (maxc > t) rounds += maxc - t;
                     if (maxc >= cap + 1) status = ST_LIVELOCK;
                     break;
@@ -238,7 +238,7 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
                 const int tn = a_next;
                 if (tn > t) {                                 // skip rounds t..tn-1
                     const int E = min(tn, cap + 1);
-                    if (E > t) peak = max(peak, prof_max(P0, P1, min(E - t, 64)));
+                    if (E > t) peak = max(peak, prof_max_lane(P0, P1, min(E - t, 64)));
                     rounds += max(0, min(tn, maxc) - t);
                     if (tn > cap) { status = ST_LIVELOCK; break; }
                     prof_shift(P0, P1, tn - t);
@@ -283,7 +283,7 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
             }
             if (h == KV_INF) {                 // R empty, S non-empty: one plain round
                 if (maxc > t) ++rounds;
-                peak = max(peak, __shfl_sync(KV_FULL, P0, 0));
+                if (lane == 0) peak = max(peak, P0);
                 prof_shift1(P0, P1);
                 ++t;
                 continue;
@@ -342,12 +342,11 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
         }
         // rounds t .. t+jump-1: decision rounds (R non-empty), batch memory Prof(t+1..t+jump)
         drounds += jump;
-        rounds += jump;
         if (jump == 1) {
-            peak = max(peak, __shfl_sync(KV_FULL, P0, 0));               // Mem(t+1)
+            if (lane == 0) peak = max(peak, P0);                          // Mem(t+1)
             prof_shift1(P0, P1);
         } else {
-            peak = max(peak, prof_max(P0, P1, jump));
+            peak = max(peak, prof_max_lane(P0, P1, jump));
             prof_shift(P0, P1, jump);
         }
         t += jump;
@@ -366,10 +365,10 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
     }
     sumc = warp_sum_i64(sumc);
     res.tel = sumc - suma;
-    res.rounds = rounds;
+    res.rounds = rounds + drounds;
     res.decision_rounds = drounds;
     res.makespan = maxc;
-    res.peak = peak;
+    res.peak = warp_max_i32(peak);
     res.status = status;
     write_result(P, inst, res);
 }
