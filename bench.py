@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-also", action="store_true",
+                    help="skip the secondary configs[1] (C2) measurement carried in the line")
     ap.add_argument("--ab", action="store_true",
                     help="also time SCHED_FLAG_PER_ROUND (one Eq. 5 evaluation per round)")
     return ap.parse_args()
@@ -70,7 +72,7 @@ def make_workload(name: str, n: int, rank: int):
         n = n or 20_000
         return W.c4(n, seed=4 + 1000 * rank), dict(workload="C4 trace-shaped n=1000 lambda=2/round M=16492",
                                                    instances_per_gpu=n, requests_per_instance=1000)
-    n = n or 512
+    n = n or 4096
     return W.c3(n, seed=3 + 1000 * rank), dict(workload="C3 trace-shaped n=10^4 lambda=2/round M=16492",
                                                instances_per_gpu=n, requests_per_instance=10_000)
 
@@ -325,22 +327,29 @@ def main():
     e2e = None
     if not args.no_e2e and world >= 1:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_off, h_req, h_mem = pin(batch.offset), pin(batch.req), pin(batch.mem)
+        # rows on the wire as uint16 deltas (SCHED_REQ_U16X4_DELTA) when they fit: half the
+        # PCIe bytes; the results read back are the schedule (completion per request) and
+        # the per-instance outputs (start = completion - o is not copied)
+        pk = batch.packed_u16()
+        fmt = K.kvsched.REQ_U16X4_DELTA if pk is not None else K.kvsched.REQ_I32X4
+        rows = pk.view(np.int16) if pk is not None else batch.req
+        e2e_fields = [k for k in fields if k != "start"]
+        h_off, h_req, h_mem = pin(batch.offset), pin(rows), pin(batch.mem)
         h_out = {}
-        for k in fields:
+        for k in e2e_fields:
             n = batch.n_req if k in ("completion", "start") else batch.n_inst
             dt = torch.int64 if k in K.kvsched.OUT_I64 else torch.int32
             h_out[k] = torch.empty(max(n, 1), dtype=dt).pin_memory()
         host = {k: v.numpy() for k, v in h_out.items()}
         a_off, a_req, a_mem = h_off.numpy(), h_req.numpy(), h_mem.numpy()
-        ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints)      # warm
+        ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints, req_format=fmt)      # warm
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.e2e_steps):
-            ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints)
+            ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints, req_format=fmt)
         f1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
@@ -348,11 +357,12 @@ def main():
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e_ms = float(e_ms.item())
         same = np.array_equal(host["rounds"][:batch.n_inst], out["rounds"][:batch.n_inst].cpu().numpy())
-        h2d = batch.n_req * 16 + (batch.n_inst + 1) * 8 + batch.n_inst * 4
-        d2h = algorithmic_bytes(batch, fields) - h2d
+        h2d = rows.nbytes + (batch.n_inst + 1) * 8 + batch.n_inst * 4
+        d2h = sum(v.numel() * v.element_size() for v in h_out.values())
         e2e = {"value": rounds_all * args.e2e_steps / (e_ms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "ms_per_step": e_ms / args.e2e_steps, "matches_device_run": bool(same)}
+               "ms_per_step": e_ms / args.e2e_steps, "matches_device_run": bool(same),
+               "req_format": "u16x4-delta" if pk is not None else "i32x4", "outputs": e2e_fields}
 
     ab = None
     if args.ab:
@@ -370,6 +380,37 @@ def main():
               "per_round_value": rounds_rank * world / (ab_ms / 1000.0),
               "speedup_of_default": ab_ms / (ms_max / args.steps)}
 
+    # configs[1] (C2, AM1: 10^4 instances of 1000 requests at t=0, M=40) under the same
+    # protocol, reported beside the primary workload
+    also = None
+    if not args.no_also and args.workload == "c5" and args.policy == "mcsf":
+        b2, cfg2 = make_workload("c2", 0, rank)
+        o2, r2, m2 = K.to_device(b2, dev)
+        out2 = K.alloc_outputs(b2.n_inst, b2.n_req, dev, fields)
+        h2 = K.hints_of(b2)
+        for _ in range(max(args.warmup, 1)):
+            ctx.run(o2, r2, m2, pol, out2, id0=rank * b2.n_inst, hints=h2)
+        torch.cuda.synchronize(dev)
+        rounds2 = int(out2["rounds"][:b2.n_inst].clamp(min=0).sum().item())
+        if world > 1:
+            dist.barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.steps):
+            ctx.run(o2, r2, m2, pol, out2, id0=rank * b2.n_inst, hints=h2)
+        h1.record(stream)
+        torch.cuda.synchronize(dev)
+        t2 = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+        n2 = torch.tensor([rounds2], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+            dist.all_reduce(n2)
+        ms2 = float(t2.item())
+        also = {"C2": {"workload": cfg2["workload"], "instances_per_gpu": b2.n_inst,
+                       "value": int(n2.item()) * args.steps / (ms2 / 1e3), "unit": UNIT,
+                       "ms_per_step": ms2 / args.steps, "kernel": ctx.last_kernel()}}
+        del o2, r2, m2, out2
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(batch, args.policy, args.cpu_seconds, gid0=id0)
@@ -385,7 +426,7 @@ def main():
                 "config": cfg, "instances_per_s": inst_all * args.steps / (ms_max / 1000.0),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
                 "gpu_launches": st["launches"], "decision_rounds_per_step": drounds_rank * world,
-                "ab": ab}
+                "ab": ab, "other_configs": also}
         print(json.dumps(line))
     ctx.close()
     if world > 1:

@@ -98,14 +98,21 @@ typedef struct {
     const int32_t *req;         /* [n_req][4] rows {a_i, s_i, o_i, o~_i}, 16-byte aligned;
                                    rows of an instance sorted by a (non-decreasing); the row
                                    position inside the instance is the request id idx and
-                                   the tie-break of every order (DESIGN Q5)                  */
+                                   the tie-break of every order (DESIGN Q5).  With req_format
+                                   SCHED_REQ_U16X4_DELTA the rows are uint16 {a_i - a_(i-1)
+                                   (a_(-1) = 0), s_i, o_i, o~_i}, 8-byte aligned             */
     const int32_t *mem_limit;   /* [n_instances] budget M of each instance           */
     int64_t instance_id0;       /* global id of instance 0 (shards; alpha-beta RNG key gid)  */
     int32_t max_requests;       /* upper bound on requests per instance, or 0 = measure      */
     int32_t max_mem;            /* upper bound on M, or 0 = measure                          */
     int32_t max_len;            /* upper bound on max(o_i, o~_i), or 0 = measure             */
-    int32_t reserved;           /* must be 0                                                 */
+    int32_t req_format;         /* SCHED_REQ_I32X4 (0) or SCHED_REQ_U16X4_DELTA (1): half the
+                                   bytes to move; decoded on the device before the run (the
+                                   device-pointer call then synchronises once to read the row
+                                   count).  Not accepted by sched_latency / sched_lb_sorted.  */
 } sched_instances;
+
+enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1 };
 /* "measure" runs a reduction kernel and synchronises the stream to read the bounds.
  * Instances that exceed a caller-given bound get status SCHED_INST_UNSUPPORTED.            */
 

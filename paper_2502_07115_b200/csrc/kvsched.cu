@@ -43,7 +43,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan;
+    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -161,6 +161,32 @@ __global__ void __launch_bounds__(128) k_latency(long long n_inst, const long lo
     }
 }
 
+// SCHED_REQ_U16X4_DELTA -> int32 rows: one warp per instance, a_i = prefix sum of the gaps.
+// Rows of instance k are input rows offset[k]-row_base.. and output rows likewise.
+__global__ void __launch_bounds__(128) k_decode_u16(long long n_inst, const long long *offset, long long row_base,
+                                                    const ushort4 *in, int4 *out)
+{
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_inst; k += warps) {
+        const long long lo = offset[k] - row_base, hi = offset[k + 1] - row_base;
+        int carry = 0;
+        for (long long b = lo; b < hi; b += 32) {
+            const long long i = b + lane;
+            const ushort4 r = i < hi ? in[i] : make_ushort4(0, 0, 0, 0);
+            int a = r.x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(KV_FULL, a, d);
+                if (lane >= d) a += y;
+            }
+            a += carry;
+            if (i < hi) out[i] = make_int4(a, r.y, r.z, r.w);
+            carry = __shfl_sync(KV_FULL, a, 31);
+        }
+    }
+}
+
 // Instances handed to a full-ring rerun that cannot run: status UNSUPPORTED, no schedule.
 __global__ void k_mark_unsupported(const KParams P, const long long *list, const unsigned long long *count)
 {
@@ -236,11 +262,13 @@ int check_common(sched_ctx *c, const sched_instances *inst)
     if (!c) return SCHED_E_STATE;
     if (!inst) return fail(c, SCHED_E_ARG, "inst is NULL");
     if (inst->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
-    if (inst->reserved != 0) return fail(c, SCHED_E_ARG, "sched_instances.reserved must be 0");
+    if (inst->req_format != SCHED_REQ_I32X4 && inst->req_format != SCHED_REQ_U16X4_DELTA)
+        return fail(c, SCHED_E_ARG, "unknown req_format %d", inst->req_format);
     if (inst->n_instances > 0) {
         if (!inst->req_offset || !inst->mem_limit || !inst->req)
             return fail(c, SCHED_E_ARG, "req_offset, req and mem_limit must be non-NULL");
-        if (((uintptr_t)inst->req) & 15u) return fail(c, SCHED_E_ARG, "req must be 16-byte aligned");
+        if (((uintptr_t)inst->req) & (inst->req_format == SCHED_REQ_I32X4 ? 15u : 7u))
+            return fail(c, SCHED_E_ARG, "req is misaligned for its format");
     }
     if (inst->max_requests < 0 || inst->max_mem < 0 || inst->max_len < 0)
         return fail(c, SCHED_E_ARG, "size hints must be >= 0");
@@ -482,6 +510,23 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
     if (inst->n_instances == 0) return SCHED_OK;
     DeviceGuard g(c->device);
+    if (inst->req_format == SCHED_REQ_U16X4_DELTA) {
+        long long n_req = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(&n_req, inst->req_offset + inst->n_instances, 8, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        if ((rc = grow(c, c->dec, (size_t)(n_req > 0 ? n_req : 1) * 16))) return rc;
+        long long blocks = (inst->n_instances + 3) / 4;
+        if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
+        k_decode_u16<<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
+                                                          0, reinterpret_cast<const ushort4 *>(inst->req),
+                                                          reinterpret_cast<int4 *>(c->dec.p));
+        CUDA_TRY(c, cudaGetLastError());
+        c->launches++;
+        sched_instances di = *inst;
+        di.req = (const int32_t *)c->dec.p;
+        di.req_format = SCHED_REQ_I32X4;
+        return run_impl(c, &di, pol, out, 0);
+    }
     return run_impl(c, inst, pol, out, 0);
 }
 
@@ -511,9 +556,18 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         }
         if (hi.max_len == 0)
             for (long long i = 0; i < n_req; ++i) {
-                const int32_t *r = inst->req + 4 * i;
-                ml = r[2] > ml ? r[2] : ml;
-                ml = r[3] > ml ? r[3] : ml;
+                long long o_, w_;
+                if (inst->req_format == SCHED_REQ_U16X4_DELTA) {
+                    const uint16_t *r = reinterpret_cast<const uint16_t *>(inst->req) + 4 * i;
+                    o_ = r[2];
+                    w_ = r[3];
+                } else {
+                    const int32_t *r = inst->req + 4 * i;
+                    o_ = r[2];
+                    w_ = r[3];
+                }
+                ml = o_ > ml ? o_ : ml;
+                ml = w_ > ml ? w_ : ml;
             }
         if (hi.max_requests == 0) hi.max_requests = (int32_t)(mr < 0x7fffffff ? mr : 0x7fffffff);
         if (hi.max_mem == 0) hi.max_mem = (int32_t)mm;
@@ -522,9 +576,12 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         if (hi.max_mem == 0) hi.max_mem = 1;
         if (hi.max_len == 0) hi.max_len = 1;
     }
+    const bool packed = inst->req_format == SCHED_REQ_U16X4_DELTA;
+    const size_t row_in = packed ? 8 : 16;                // bytes per input row on the wire
     const size_t b_off = (size_t)(ni + 1) * 8, b_req = (size_t)n_req * 16, b_mem = (size_t)ni * 4;
     if ((rc = grow(c, c->h_off, b_off)) || (rc = grow(c, c->h_req, b_req)) || (rc = grow(c, c->h_mem, b_mem)))
         return rc;
+    if (packed && (rc = grow(c, c->h_pk, (size_t)n_req * 8 + 8))) return rc;
     // device outputs: completion, start [n_req] int32; 4 x int64 + 3 x int32 per instance
     const size_t o_comp = 0, o_start = o_comp + (size_t)n_req * 4, o_i64 = (o_start + (size_t)n_req * 4 + 15) & ~(size_t)15;
     const size_t o_i32 = o_i64 + (size_t)ni * 8 * 4;
@@ -554,12 +611,23 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     for (long long k = 0; k < n_chunks; ++k) {
         const long long i0 = ni * k / n_chunks, i1 = ni * (k + 1) / n_chunks;
         const long long r0 = hoff[i0], r1 = hoff[i1];
+        char *dst = packed ? (char *)c->h_pk.p + r0 * 8 : (char *)c->h_req.p + r0 * 16;
+        const char *src = (const char *)inst->req + r0 * row_in;
         if (r1 > r0)
-            CUDA_TRY(c, cudaMemcpyAsync((char *)c->h_req.p + r0 * 16, inst->req + 4 * r0, (size_t)(r1 - r0) * 16,
-                                        cudaMemcpyHostToDevice, c->s_in));
+            CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)(r1 - r0) * row_in, cudaMemcpyHostToDevice, c->s_in));
         CUDA_TRY(c, cudaEventRecord(ev[2 * k], c->s_in));
         CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2 * k], 0));
+        if (packed && i1 > i0) {
+            long long blocks = (i1 - i0 + 3) / 4;
+            if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
+            k_decode_u16<<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
+                                                              reinterpret_cast<const ushort4 *>(dst),
+                                                              reinterpret_cast<int4 *>((char *)c->h_req.p + r0 * 16));
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        }
         sched_instances di = hi;
+        di.req_format = SCHED_REQ_I32X4;
         di.n_instances = i1 - i0;
         di.req_offset = (const int64_t *)(doff + i0);
         di.req = (const int32_t *)((char *)c->h_req.p + r0 * 16);
@@ -607,6 +675,7 @@ int sched_latency(sched_ctx *c, const sched_instances *inst, const int32_t *comp
     if (inst->n_instances == 0) return SCHED_OK;
     if (!inst->req_offset || !inst->req || !completion)
         return fail(c, SCHED_E_ARG, "req_offset, req and completion must be non-NULL");
+    if (inst->req_format != SCHED_REQ_I32X4) return fail(c, SCHED_E_ARG, "sched_latency takes SCHED_REQ_I32X4 rows");
     long long blocks = (inst->n_instances + 3) / 4;
     if (blocks > 16LL * c->num_sms) blocks = 16LL * c->num_sms;
     k_latency<<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances,
@@ -624,6 +693,7 @@ int sched_lb_sorted(sched_ctx *c, const sched_instances *inst, int64_t *lb)
     int rc = check_common(c, inst);
     if (rc) return rc;
     if (!lb) return fail(c, SCHED_E_ARG, "lb is NULL");
+    if (inst->req_format != SCHED_REQ_I32X4) return fail(c, SCHED_E_ARG, "sched_lb_sorted takes SCHED_REQ_I32X4 rows");
     if (inst->n_instances == 0) return SCHED_OK;
     DeviceGuard g(c->device);
     int max_n = inst->max_requests;
@@ -775,7 +845,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {

@@ -20,6 +20,7 @@ POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": A
               "mcsf_protected": MCSF_PROTECTED}
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
+REQ_I32X4, REQ_U16X4_DELTA = 0, 1
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}
 
 # every symbol include/kvsched.h declares
@@ -37,7 +38,7 @@ i32, i64, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
 class SchedInstances(ctypes.Structure):
     _fields_ = [("n_instances", i64), ("req_offset", P), ("req", P), ("mem_limit", P),
                 ("instance_id0", i64), ("max_requests", i32), ("max_mem", i32),
-                ("max_len", i32), ("reserved", i32)]
+                ("max_len", i32), ("req_format", i32)]
 
 
 class SchedPolicy(ctypes.Structure):
@@ -158,25 +159,25 @@ class Context:
 
     # -- device path -------------------------------------------------------------------
     @staticmethod
-    def instances(offset, req, mem, id0: int = 0, hints=(0, 0, 0)) -> SchedInstances:
+    def instances(offset, req, mem, id0: int = 0, hints=(0, 0, 0), req_format: int = 0) -> SchedInstances:
         n = int(mem.shape[0])
         return SchedInstances(n, _ptr(offset), _ptr(req), _ptr(mem), int(id0), int(hints[0]),
-                              int(hints[1]), int(hints[2]), 0)
+                              int(hints[1]), int(hints[2]), int(req_format))
 
     def run(self, offset, req, mem, policy: Policy, outputs: dict, id0: int = 0,
-            hints=(0, 0, 0)) -> None:
+            hints=(0, 0, 0), req_format: int = 0) -> None:
         """sched_run_instances on device tensors; `outputs` maps OUT_FIELDS names to
         preallocated device tensors (missing = not requested)."""
-        si = self.instances(offset, req, mem, id0, hints)
+        si = self.instances(offset, req, mem, id0, hints, req_format)
         so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS])
         pc = policy.as_c()
         self._check(self._lib.sched_run_instances(self._h, ctypes.byref(si), ctypes.byref(pc),
                                                   ctypes.byref(so)), "sched_run_instances")
 
     def run_host(self, offset: np.ndarray, req: np.ndarray, mem: np.ndarray, policy: Policy,
-                 outputs: dict, id0: int = 0, hints=(0, 0, 0)) -> None:
+                 outputs: dict, id0: int = 0, hints=(0, 0, 0), req_format: int = 0) -> None:
         """sched_run_instances_host on host (numpy, ideally pinned) arrays."""
-        si = self.instances(offset, req, mem, id0, hints)
+        si = self.instances(offset, req, mem, id0, hints, req_format)
         so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS])
         pc = policy.as_c()
         self._check(self._lib.sched_run_instances_host(self._h, ctypes.byref(si), ctypes.byref(pc),
@@ -265,13 +266,23 @@ def hints_of(batch) -> tuple[int, int, int]:
     return (max(batch.max_requests(), 1), max(batch.max_mem(), 1), max(batch.max_len(), 1))
 
 
-def simulate(ctx: Context, batch, policy: Policy, id0: int = 0, hints=None, fields=OUT_FIELDS) -> dict:
-    """Run a host batch on the device; returns numpy arrays trimmed to the batch size."""
+def simulate(ctx: Context, batch, policy: Policy, id0: int = 0, hints=None, fields=OUT_FIELDS,
+             packed: bool = False) -> dict:
+    """Run a host batch on the device; returns numpy arrays trimmed to the batch size.
+    packed=True ships the rows as SCHED_REQ_U16X4_DELTA (decoded on the device)."""
     import torch
     dev = torch.device("cuda", ctx.device)
     off, req, mem = to_device(batch, dev)
+    fmt = REQ_I32X4
+    if packed:
+        pk = batch.packed_u16()
+        if pk is None:
+            raise ValueError("batch does not fit the uint16 delta encoding")
+        req = torch.from_numpy(pk.view(np.int16) if pk.size else np.zeros((1, 4), np.int16)).to(dev)
+        fmt = REQ_U16X4_DELTA
     out = alloc_outputs(batch.n_inst, batch.n_req, dev, fields)
-    ctx.run(off, req, mem, policy, out, id0=id0, hints=hints if hints is not None else (0, 0, 0))
+    ctx.run(off, req, mem, policy, out, id0=id0, hints=hints if hints is not None else (0, 0, 0),
+            req_format=fmt)
     torch.cuda.synchronize(dev)
     res = {}
     for k, v in out.items():

@@ -456,6 +456,29 @@ def test_host_path_pipelined_chunks(K, ctx, oracle_mod, pol, monkeypatch):
     assert_parity(o, outs0, b, "host chunks, measured hints")
 
 
+@pytest.mark.parametrize("pol", [0, 1, 2, 4])
+def test_packed_u16_rows(K, ctx, oracle_mod, pol, monkeypatch):
+    """SCHED_REQ_U16X4_DELTA rows (half the bytes), decoded on the device, through both the
+    device-pointer call and the chunked host path, give the same bytes as int32 rows."""
+    import paper_2502_07115_b200.kvsched as kv
+    b = W.random_small(1500, 90 + pol, n_max=50, M_lo=6, M_hi=120, a_max=300)
+    if pol == 4:
+        b = W.with_prediction_noise(b, 0.3, seed=2)
+    kw = dict(alpha=(1, 10)) if pol >= 2 else {}
+    o = oracle_run(oracle_mod, b, pol, **kw)
+    p = K.Policy(KIND[pol], kw.get("alpha", (0, 1)))
+    g = K.simulate(ctx, b, p, hints=K.hints_of(b), packed=True)
+    assert_parity(o, g, b, "packed, device")
+    monkeypatch.setenv("KVSCHED_HOST_CHUNK_ROWS", "1024")
+    pk = b.packed_u16()
+    outs = _host_outputs(b)
+    ctx.run_host(b.offset, pk, b.mem, p, outs, hints=K.hints_of(b), req_format=kv.REQ_U16X4_DELTA)
+    assert_parity(o, outs, b, "packed, host chunks")
+    outs = _host_outputs(b)
+    ctx.run_host(b.offset, pk, b.mem, p, outs, req_format=kv.REQ_U16X4_DELTA)      # host-measured hints
+    assert_parity(o, outs, b, "packed, host, measured hints")
+
+
 def test_host_path(K, ctx, oracle_mod):
     """sched_run_instances_host (host buffers, copies inside the call) gives the same bytes."""
     import paper_2502_07115_b200.kvsched as kv

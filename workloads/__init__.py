@@ -82,6 +82,20 @@ class Batch:
         return Batch(off, np.ascontiguousarray(req, dtype=np.int32),
                      np.ascontiguousarray(self.mem[ks]), self.name + "[subset]", dict(self.meta))
 
+    def packed_u16(self):
+        """Rows as uint16 {a_i - a_(i-1) (a_(-1) = 0 per instance), s, o, o~} (the C ABI's
+        SCHED_REQ_U16X4_DELTA), or None if a value does not fit 16 bits."""
+        if self.n_req == 0:
+            return np.zeros((0, 4), np.uint16)
+        a = self.req[:, 0].astype(np.int64)
+        gap = np.diff(a, prepend=0)
+        starts = self.offset[:-1][self.sizes() > 0]
+        gap[starts] = a[starts]
+        cols = np.stack([gap, self.req[:, 1], self.req[:, 2], self.req[:, 3]], 1)
+        if cols.min() < 0 or cols.max() > 0xFFFF:
+            return None
+        return np.ascontiguousarray(cols.astype(np.uint16))
+
     def sha256(self) -> str:
         h = hashlib.sha256()
         for a in (self.offset, self.req, self.mem):
