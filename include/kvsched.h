@@ -177,6 +177,28 @@ int sched_latency(sched_ctx *ctx, const sched_instances *inst, const int32_t *co
  * inst->max_requests as a hint (0 = measure).                                            */
 int sched_lb_sorted(sched_ctx *ctx, const sched_instances *inst, int64_t *lb);
 
+/* Wall clock of a schedule under an affine batch time (SPEC's DurationModel, standing in for
+ * the Vidur timing of P:459; DESIGN Q28).  Feasibility stays in rounds; round r (first arrival
+ * r0 <= r < makespan) processes tokens(r) = sum_{p_i = r} s_i + #{i : p_i < r < c_i} and lasts
+ * c0 + c1 tokens(r); W(r0) = 0.  Per instance k (device pointers; any output may be NULL):
+ *   tel_wall[k] = sum_i W(c_i) - W(a_i); makespan_wall[k] = W(max_i c_i)   (-1 if a request
+ *   has no schedule, i.e. start or completion < 0);
+ *   bins[k][b] = sum of tokens(r) over rounds with floor(W(r) / bin_width) = b < n_bins
+ *   (per-bin throughput, Fig. 5);
+ *   mem_trace[k][j] = sum_{i: p_i <= r < c_i} (s_i + r + 1 - p_i), r = r0 + j < makespan,
+ *   0 beyond (memory over time, Figs. 6 and 9).
+ * start / completion are the outputs of sched_run_instances for `inst` (I32X4 rows).      */
+typedef struct {
+    int64_t c0, c1;             /* batch time c0 + c1 tokens, integer time units (> 0)      */
+    int64_t bin_width;          /* throughput bin width in time units (0 = no bins)         */
+    int32_t n_bins;             /* bins per instance                                        */
+    int32_t trace_len;          /* memory-trace rounds per instance                         */
+} sched_clock;
+
+int sched_wallclock(sched_ctx *ctx, const sched_instances *inst, const int32_t *start,
+                    const int32_t *completion, const sched_clock *clk, int64_t *tel_wall,
+                    int64_t *makespan_wall, int64_t *bins, int32_t *mem_trace);
+
 /* On-device generation of Arrival-Model-2 instances on a lambda x M sweep grid
  * (configuration C5), from an integer counter-based specification; the bytes equal those of
  * the host reference workloads.am2_counter.  Instance k (global id g = instance_id0 + k):

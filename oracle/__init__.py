@@ -65,6 +65,8 @@ def lib():
         L.or_opt_bruteforce.restype = i64
         L.or_lb_sorted.argtypes = [i64, P, i32]
         L.or_lb_sorted.restype = i64
+        L.or_wallclock.argtypes = [i64, P, P, P, i64, i64, i64, i32, i32, P, P, P, P]
+        L.or_wallclock.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -182,3 +184,18 @@ def lb_sorted(req, M: int) -> int:
     """Volume lower bound on OPT for all-at-0 instances (P:212, P:319 argument)."""
     r = _req(req)
     return int(lib().or_lb_sorted(r.shape[0], _ptr(r), int(M)))
+
+
+def wallclock(req, start, completion, c0: int, c1: int, bin_width: int = 0, n_bins: int = 0,
+              trace_len: int = 0) -> dict:
+    """NEXT-4: wall clock of a schedule under the affine batch time c0 + c1 tokens (DESIGN Q28)."""
+    r = _req(req)
+    st = np.ascontiguousarray(np.asarray(start, dtype=np.int32))
+    cp = np.ascontiguousarray(np.asarray(completion, dtype=np.int32))
+    bins = np.zeros(max(n_bins, 1), np.int64)
+    mem = np.zeros(max(trace_len, 1), np.int32)
+    tw, mw = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    rc = lib().or_wallclock(r.shape[0], _ptr(r), _ptr(st), _ptr(cp), int(c0), int(c1), int(bin_width),
+                            int(n_bins), int(trace_len), _ptr(tw), _ptr(mw), _ptr(bins), _ptr(mem))
+    return dict(ok=rc == 0, tel_wall=int(tw[0]), makespan_wall=int(mw[0]), bins=bins[:n_bins],
+                mem=mem[:trace_len])

@@ -612,3 +612,53 @@ int64_t or_lb_sorted(int64_t n, const int32_t *req, int32_t M)
     free(vol); free(os);
     return lb;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-4: the wall clock of a schedule under an affine batch time (SPEC's DurationModel, */
+/* the stand-in for the Vidur timing of P:459; DESIGN Q28).  Feasibility stays in rounds; */
+/* round r (r0 = a_0 <= r < makespan) processes tokens(r) = sum_{p_i = r} s_i (prefill) + */
+/* #{i : p_i < r < c_i} (one decode token each) and lasts c0 + c1 tokens(r).  W(r) = the  */
+/* start time of round r, W(r0) = 0.  Outputs: tel_wall = sum_i W(c_i) - W(a_i),        */
+/* makespan_wall = W(max c); tokens of round r counted in bin floor(W(r) / bin_width)     */
+/* (bins >= n_bins dropped); mem[j] = sum_{i: p_i <= r < c_i} (s_i + r + 1 - p_i) for     */
+/* r = r0 + j (the batch memory of round r), j < trace_len.  Plain round-by-round loop.   */
+/* Returns -1 if some request is unscheduled (c < 0).                                     */
+/* ------------------------------------------------------------------------------------ */
+int or_wallclock(int64_t n, const int32_t *req, const int32_t *start, const int32_t *completion,
+                 int64_t c0, int64_t c1, int64_t bin_width, int32_t n_bins, int32_t trace_len,
+                 int64_t *tel_wall, int64_t *makespan_wall, int64_t *bins, int32_t *mem)
+{
+    for (int32_t b = 0; b < n_bins; b++) bins[b] = 0;
+    for (int32_t j = 0; j < trace_len; j++) mem[j] = 0;
+    *tel_wall = 0;
+    *makespan_wall = 0;
+    if (n == 0) return 0;
+    int64_t r0 = req[0], rend = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (completion[i] < 0 || start[i] < 0) return -1;
+        if (completion[i] > rend) rend = completion[i];
+    }
+    /* W(r) for r0 <= r <= rend */
+    int64_t *W = malloc(sizeof(int64_t) * (size_t)(rend - r0 + 2));
+    W[0] = 0;
+    for (int64_t r = r0; r < rend; r++) {
+        int64_t tokens = 0, m = 0;
+        for (int64_t i = 0; i < n; i++) {
+            int64_t p = start[i], c = completion[i], s = req[4 * i + 1];
+            if (p == r) tokens += s;                       /* prefill */
+            else if (p < r && r < c) tokens += 1;          /* one decode token */
+            if (p <= r && r < c) m += s + r + 1 - p;       /* batch memory (Eq. 3 at r+1) */
+        }
+        W[r - r0 + 1] = W[r - r0] + c0 + c1 * tokens;
+        if (bin_width > 0) {
+            int64_t b = W[r - r0] / bin_width;
+            if (b < n_bins) bins[b] += tokens;
+        }
+        if (r - r0 < trace_len) mem[r - r0] = (int32_t)m;
+    }
+    for (int64_t i = 0; i < n; i++)
+        *tel_wall += W[completion[i] - r0] - W[req[4 * i] - r0];
+    *makespan_wall = W[rend - r0];
+    free(W);
+    return 0;
+}

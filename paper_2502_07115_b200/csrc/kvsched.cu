@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/kvsched.h"
+#include "kernel_clock.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_lb.cuh"
 #include "kernel_prot.cuh"
@@ -719,6 +720,33 @@ int sched_lb_sorted(sched_ctx *c, const sched_instances *inst, int64_t *lb)
     k_lb_sorted<<<(int)blocks, 512, smem, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
                                                         reinterpret_cast<const int4 *>(inst->req), inst->mem_limit, max_n,
                                                         reinterpret_cast<long long *>(lb));
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
+int sched_wallclock(sched_ctx *c, const sched_instances *inst, const int32_t *start, const int32_t *completion,
+                    const sched_clock *clk, int64_t *tel_wall, int64_t *makespan_wall, int64_t *bins, int32_t *mem_trace)
+{
+    int rc = check_common(c, inst);
+    if (rc) return rc;
+    if (!clk) return fail(c, SCHED_E_ARG, "clk is NULL");
+    if (inst->req_format != SCHED_REQ_I32X4) return fail(c, SCHED_E_ARG, "sched_wallclock takes SCHED_REQ_I32X4 rows");
+    if (clk->c0 < 1 || clk->c1 < 0 || clk->bin_width < 0 || clk->n_bins < 0 || clk->trace_len < 0)
+        return fail(c, SCHED_E_ARG, "need c0 >= 1, c1 >= 0, bin_width, n_bins, trace_len >= 0");
+    if (inst->n_instances == 0) return SCHED_OK;
+    if (!start || !completion) return fail(c, SCHED_E_ARG, "start and completion are required");
+    DeviceGuard g(c->device);
+    ClockParams C{inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
+                  reinterpret_cast<const int4 *>(inst->req), start, completion, clk->c0, clk->c1, clk->bin_width,
+                  clk->n_bins, clk->trace_len, reinterpret_cast<long long *>(tel_wall),
+                  reinterpret_cast<long long *>(makespan_wall), bins && clk->n_bins > 0 ? reinterpret_cast<long long *>(bins) : nullptr,
+                  mem_trace && clk->trace_len > 0 ? mem_trace : nullptr};
+    const int smem = 4 * (int)sizeof(ClockSmem);
+    CUDA_TRY(c, cudaFuncSetAttribute(k_wallclock, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    long long blocks = (inst->n_instances + 3) / 4;
+    if (blocks > 16LL * c->num_sms) blocks = 16LL * c->num_sms;
+    k_wallclock<<<(int)blocks, 128, smem, c->stream>>>(C);
     CUDA_TRY(c, cudaGetLastError());
     c->launches++;
     return SCHED_OK;

@@ -26,7 +26,7 @@ ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED
 # every symbol include/kvsched.h declares
 EXPORTS = ("sched_abi_version", "sched_init", "sched_set_stream", "sched_run_instances",
            "sched_run_instances_host", "sched_latency", "sched_lb_sorted", "sched_gen_am2_count",
-           "sched_gen_am2_fill", "sched_philox4x32_10",
+           "sched_gen_am2_fill", "sched_wallclock", "sched_philox4x32_10",
            "sched_set_timing",
            "sched_get_stats", "sched_reset_stats", "sched_last_kernel", "sched_finalize",
            "sched_last_error")
@@ -50,6 +50,10 @@ class SchedGenAm2(ctypes.Structure):
     _fields_ = [("n_instances", i64), ("instance_id0", i64), ("seed", u64), ("n_lambda", i32),
                 ("n_m", i32), ("poisson_cdf", P), ("m_values", P), ("T_lo", i32), ("T_hi", i32),
                 ("s_lo", i32), ("s_hi", i32)]
+
+
+class SchedClock(ctypes.Structure):
+    _fields_ = [("c0", i64), ("c1", i64), ("bin_width", i64), ("n_bins", i32), ("trace_len", i32)]
 
 
 class SchedOutputs(ctypes.Structure):
@@ -85,6 +89,8 @@ def load() -> ctypes.CDLL:
         L.sched_philox4x32_10.argtypes = [P, i64, P, P, P]
         L.sched_lb_sorted.argtypes = [P, ctypes.POINTER(SchedInstances), P]
         L.sched_gen_am2_count.argtypes = [P, ctypes.POINTER(SchedGenAm2), P]
+        L.sched_wallclock.argtypes = [P, ctypes.POINTER(SchedInstances), P, P, ctypes.POINTER(SchedClock),
+                                      P, P, P, P]
         L.sched_gen_am2_fill.argtypes = [P, ctypes.POINTER(SchedGenAm2), P, P, P]
         L.sched_set_timing.argtypes = [P, ctypes.c_int]
         L.sched_get_stats.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
@@ -193,6 +199,24 @@ class Context:
         """sched_lb_sorted: lb[k] = volume lower bound on OPT of simultaneous-arrival instances."""
         si = self.instances(offset, req, mem, 0, hints)
         self._check(self._lib.sched_lb_sorted(self._h, ctypes.byref(si), _ptr(lb)), "sched_lb_sorted")
+
+    def wallclock(self, offset, req, mem, start, completion, c0: int, c1: int, bin_width: int = 0,
+                  n_bins: int = 0, trace_len: int = 0) -> dict:
+        """NEXT-4: wall clock of a schedule (sched_wallclock); returns device tensors."""
+        import torch
+        dev = start.device
+        n = int(offset.shape[0]) - 1
+        out = dict(tel_wall=torch.empty(max(n, 1), dtype=torch.int64, device=dev),
+                   makespan_wall=torch.empty(max(n, 1), dtype=torch.int64, device=dev),
+                   bins=torch.empty((max(n, 1), max(n_bins, 1)), dtype=torch.int64, device=dev),
+                   mem=torch.empty((max(n, 1), max(trace_len, 1)), dtype=torch.int32, device=dev))
+        si = self.instances(offset, req, mem)
+        ck = SchedClock(int(c0), int(c1), int(bin_width), int(n_bins), int(trace_len))
+        self._check(self._lib.sched_wallclock(self._h, ctypes.byref(si), _ptr(start), _ptr(completion), ctypes.byref(ck),
+                                              _ptr(out["tel_wall"]), _ptr(out["makespan_wall"]),
+                                              _ptr(out["bins"]) if n_bins else None,
+                                              _ptr(out["mem"]) if trace_len else None), "sched_wallclock")
+        return out
 
     def gen_am2(self, n_inst: int, spec, id0: int = 0):
         """NEXT-3: generate an AM2-grid batch on the device (sched_gen_am2_count + _fill).

@@ -388,6 +388,34 @@ def test_device_generation_edge_specs(K, ctx):
         assert np.array_equal(req.cpu().numpy()[:n_req], h.req[:n_req])
 
 
+@pytest.mark.parametrize("maker", ["c5", "c4", "fuzz", "c3"])
+def test_wallclock_kernel(K, ctx, oracle_mod, maker):
+    """NEXT-4: sched_wallclock on GPU schedules equals the oracle's round-by-round clock."""
+    import torch
+    b = {"c5": lambda: W.am2(400, 61), "c4": lambda: W.c4(8, 62),
+         "fuzz": lambda: W.random_small(300, 63, n_max=40, M_lo=6, M_hi=200, a_max=700),
+         "c3": lambda: W.c3(1, 64, 2.0)}[maker]()
+    dev = torch.device("cuda", 0)
+    off, req, mem = K.to_device(b, dev)
+    out = K.alloc_outputs(b.n_inst, b.n_req, dev)
+    ctx.run(off, req, mem, K.Policy("mcsf"), out, hints=K.hints_of(b))
+    c0, c1, bw, nb, tl = 40, 3, 997, 64, 300
+    w = ctx.wallclock(off, req, mem, out["start"], out["completion"], c0, c1, bw, nb, tl)
+    torch.cuda.synchronize()
+    st, cp = out["start"].cpu().numpy(), out["completion"].cpu().numpy()
+    tw, mw = w["tel_wall"].cpu().numpy(), w["makespan_wall"].cpu().numpy()
+    bins, memt = w["bins"].cpu().numpy(), w["mem"].cpu().numpy()
+    for k in range(min(b.n_inst, 120)):
+        r, M = b.instance(k)
+        lo, hi = int(b.offset[k]), int(b.offset[k + 1])
+        o = oracle_mod.wallclock(r, st[lo:hi], cp[lo:hi], c0, c1, bw, nb, tl)
+        if len(r) == 0:
+            assert tw[k] == 0 and mw[k] == 0
+            continue
+        assert (tw[k], mw[k]) == (o["tel_wall"], o["makespan_wall"]), k
+        assert np.array_equal(bins[k], o["bins"]) and np.array_equal(memt[k], o["mem"]), k
+
+
 def test_lb_sorted_kernel(K, ctx, oracle_mod):
     """NEXT-2 (GPU part): the all-at-0 volume bound, bit-exact against the oracle's."""
     import torch

@@ -438,3 +438,36 @@ def test_protected_mcsf_unconstrained(oracle_mod):
         M = int(2 * (req[:, 1] + np.maximum(req[:, 2], req[:, 3])).sum())
         out = O.simulate(req, M, O.MCSF_PROT, alpha=(1, 2))
         assert out["status"] == 0 and (out["completion"] == req[:, 0] + req[:, 2]).all()
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-4: wall clock under the affine batch time (DESIGN Q28)
+# ----------------------------------------------------------------------------------------
+def test_wallclock_closed_forms(oracle_mod):
+    """A single request (s, o) arriving at 3: rounds 3..2+o, prefill s then o-1 decode tokens,
+    so W(c) = o c0 + c1 (s + o - 1); with c0 = 1, c1 = 0 the wall clock is the round count."""
+    O = oracle_mod
+    for s, o in ((1, 1), (4, 7), (9, 2)):
+        out = O.simulate([[3, s, o, o]], s + o, 0)
+        w = O.wallclock([[3, s, o, o]], out["start"], out["completion"], 5, 2, 1, 64, 16)
+        assert w["tel_wall"] == o * 5 + 2 * (s + o - 1) == w["makespan_wall"]
+        assert w["bins"].sum() == s + o - 1                       # token conservation
+        assert list(w["mem"][:o]) == [s + k for k in range(1, o + 1)]
+
+
+def test_wallclock_unit_clock_is_tel(oracle_mod):
+    """c0 = 1, c1 = 0 (one time unit per round) reproduces TEL and the makespan in rounds;
+    the memory trace's maximum is the peak; bins conserve every processed token."""
+    O = oracle_mod
+    b = W.random_small(80, 95, n_max=20, M_lo=8, M_hi=50, a_max=15)
+    for k in range(b.n_inst):
+        req, M = b.instance(k)
+        if len(req) == 0:
+            continue
+        out = O.simulate(req, M, 0)
+        span = int(out["makespan"] - req[0, 0])
+        w = O.wallclock(req, out["start"], out["completion"], 1, 0, 1, span + 1, span + 1)
+        assert w["tel_wall"] == out["tel"] and w["makespan_wall"] == span
+        assert w["mem"].max() == out["peak"]
+        w2 = O.wallclock(req, out["start"], out["completion"], 3, 1, 7, 10_000, 0)
+        assert w2["bins"].sum() == int((req[:, 1] + req[:, 2] - 1).sum())

@@ -150,6 +150,31 @@ def main():
         report[f"C4 {name}"] = r
         print("C4", name, json.dumps(r), flush=True)
 
+    # NEXT-4: wall clock of the C4 MC-SF and MC-Benchmark schedules under an affine batch time
+    # (placeholder constants: 20 ms per batch + 0.05 ms per token; only ratios are claimed)
+    dev = torch.device("cuda", 0)
+    off, req, mem = K.to_device(b, dev)
+    wall = {}
+    for kind in ("mcsf", "mcbench"):
+        out = K.alloc_outputs(b.n_inst, b.n_req, dev)
+        ctx.run(off, req, mem, K.Policy(kind), out, hints=K.hints_of(b))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        w = ctx.wallclock(off, req, mem, out["start"], out["completion"], 20_000, 50, 1_000_000, 64, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        tw = w["tel_wall"].cpu().numpy()
+        wall[kind] = {"avg_latency_s": float(tw.mean() / 1000 / 1e6), "kernel_ms": e0.elapsed_time(e1),
+                      "first_instance_tokens_per_s_first_10_bins": w["bins"][0, :10].cpu().tolist()}
+        if kind == "mcsf":
+            st, cp = out["start"][:1000].cpu().numpy(), out["completion"][:1000].cpu().numpy()
+            o = oracle.wallclock(b.req[:1000], st, cp, 20_000, 50, 1_000_000, 64, 0)
+            wall[kind]["instance0_matches_oracle"] = o["tel_wall"] == int(tw[0])
+    wall["mcsf_over_mcbench_avg_latency"] = wall["mcsf"]["avg_latency_s"] / wall["mcbench"]["avg_latency_s"]
+    report["C4 wall clock (NEXT-4)"] = wall
+    print("C4wall", json.dumps(wall), flush=True)
+
     # C5: the sweep (per grid cell mean TEL / n)
     b = W.am2(200_000 if q else 1_000_000, 5)
     pol = K.Policy("mcsf")
