@@ -35,7 +35,9 @@
  *   - Unless a function says "host", every pointer is a CUDA device pointer on the context's
  *     device, caller-owned; the library never retains or frees caller memory.
  *   - Work is enqueued asynchronously on the context's stream; nothing synchronises the host
- *     unless stated (sched_run_instances synchronises only when a size hint is 0).
+ *     unless stated (sched_run_instances synchronises when a size hint is 0, for packed rows,
+ *     and -- on the shared-memory ring path -- when n_instances x max_requests rows of scratch
+ *     would exceed 256 MB, to read the true row count).
  *   - Argument errors are detected synchronously, nothing is enqueued, a negative SCHED_E_*
  *     is returned and sched_last_error() describes it.  Per-instance data problems never
  *     fail the call: they set that instance's status (SCHED_INST_*).

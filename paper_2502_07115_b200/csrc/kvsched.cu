@@ -447,7 +447,17 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
     P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
     CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
-    const size_t slots = (size_t)inst->n_instances * (size_t)max_req;
+    // per-request scratch rows: n_instances * max_requests bounds the row count without a
+    // device read; for very ragged batches that bound is loose, so read the true count
+    size_t slots = (size_t)inst->n_instances * (size_t)max_req;
+    if (slots * 20 > ((size_t)256 << 20)) {
+        long long last = 0, first = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(&last, inst->req_offset + inst->n_instances, 8, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(&first, inst->req_offset, 8, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        const size_t rows = (size_t)(last - first > 0 ? last - first : 1);
+        if (rows < slots) slots = rows;
+    }
     const char *name = "";
     if (pol->policy == SCHED_MCSF || prot) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
