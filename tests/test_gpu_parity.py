@@ -416,6 +416,22 @@ def test_wallclock_kernel(K, ctx, oracle_mod, maker):
         assert np.array_equal(bins[k], o["bins"]) and np.array_equal(memt[k], o["mem"]), k
 
 
+@pytest.mark.parametrize("pol", [0, 2, 4])
+def test_very_ragged_batch(K, ctx, oracle_mod, pol):
+    """One 20000-request instance among 8000 tiny ones: the ring path sizes its scratch by the
+    true row count (n_instances x max_requests would be ~3 GB)."""
+    g = np.random.default_rng(85)
+    big = np.stack([np.sort(g.integers(0, 9000, 20000)), g.integers(1, 30, 20000),
+                    g.integers(1, 200, 20000), np.zeros(20000, np.int64)], 1)
+    big[:, 3] = big[:, 2]
+    small = W.random_small(8000, 86, n_max=6, M_lo=120, M_hi=300, a_max=10)
+    insts = [(big, 3000)] + [small.instance(k) for k in range(small.n_inst)]
+    b = W.from_instances(insts)
+    kw = dict(alpha=(1, 10)) if pol >= 2 else {}
+    o, g_ = check(K, ctx, oracle_mod, b, pol, "very ragged", **kw)
+    assert (o["status"][1:] == g_["status"][1:]).all()
+
+
 def test_lb_sorted_kernel(K, ctx, oracle_mod):
     """NEXT-2 (GPU part): the all-at-0 volume bound, bit-exact against the oracle's."""
     import torch
