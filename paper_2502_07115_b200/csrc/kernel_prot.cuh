@@ -78,6 +78,7 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
     const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
     const int cap = (int)min(cap64, 0x7ffffffell);
     const int B = (int)(((long long)(P.alpha_den - P.alpha_num) * M) / P.alpha_den);   // (1-alpha)M
+    const bool multi = !(P.flags & 1);                  // SCHED_FLAG_PER_ROUND: no jumps
     int *relnext = P.relnext + off;                     // chain links by idx
     int *pst = P.pstart + off;                          // start rounds by idx
 
@@ -229,6 +230,44 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
         peak = max(peak, mnow);
         mem_prev = mnow;
         ++t;
+
+        // Rounds r = t, t+1, ... in which nothing can happen, found 32 at a time: S non-empty
+        // and no overflow (0 < Mem(r+1) <= M), no early completion chained on r, no arrival
+        // that sorts before the head (any arrival if R is empty), and the head violates
+        // Eq. 5 on (1-alpha)M at r (ring_first_fit: the projection only advances meanwhile).
+        while (multi && mem_prev > 0) {
+            int d = 32;
+            if (h != KV_INF) {
+                if (hstale) { he = P.rq[off + h]; hstale = false; }
+                d = ring_first_fit(S.pp, mask, L, Gp, t, (int)he.x, (int)he.y, B);
+            }
+            if (d == 0) break;
+            int Ta = a_next;
+            if (h != KV_INF) {
+                Ta = KV_INF;
+                for (int k = next; k < n; k += 32) {
+                    const int kk = k + lane;
+                    const int ak = kk < n ? reqi[(off + kk) * 4] : KV_INF;
+                    const bool before = ak < t + 32;
+                    const uint32_t m = __ballot_sync(KV_FULL, before && P.arank[off + min(kk, n - 1)] < h);
+                    if (m) { Ta = __shfl_sync(KV_FULL, ak, __ffs(m) - 1); break; }
+                    if (!__all_sync(KV_FULL, before)) break;
+                }
+            }
+            const int r = t + lane;
+            const int v = S.pa[(r + 1) & mask];
+            const bool quiet = lane < d && r <= cap && r < Ta && v > 0 && v <= M && S.rel[r & mask] < 0;
+            const uint32_t qm = __ballot_sync(KV_FULL, quiet);
+            const int k = qm == KV_FULL ? 32 : __ffs(~qm) - 1;          // quiet rounds t..t+k-1
+            if (k == 0) break;
+            mem_prev = __shfl_sync(KV_FULL, v, k - 1);
+            peak = max(peak, ring_jump(S.pa, mask, L, Ga, t, t + k, t + k));
+            ring_jump(S.pp, mask, L, Gp, t, t, t + k);
+            rounds += k;
+            if (h != KV_INF) drounds += k;
+            t += k;
+            if (k < 32) break;
+        }
     }
 
     if (status == ST_RETRY) {

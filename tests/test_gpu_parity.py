@@ -212,16 +212,19 @@ def test_ring_window_and_long_requests(K, ctx, oracle_mod, pol, flags):
     check(K, ctx, oracle_mod, c, pol, "long-list overflow -> full ring", flags=flags, **kw)
 
 
+@pytest.mark.parametrize("flags", [0, 1])
 @pytest.mark.parametrize("eps", [0.2, 0.5, 0.8])
 @pytest.mark.parametrize("shape", ["small", "long", "c4"])
-def test_protected_mcsf(K, ctx, oracle_mod, eps, shape):
-    """NEXT-1: noisy predictions, budget (1-alpha)M, clearing on overflow."""
+def test_protected_mcsf(K, ctx, oracle_mod, eps, shape, flags):
+    """NEXT-1: noisy predictions, budget (1-alpha)M, clearing on overflow; with
+    the quiet-round jumps (flags 0) and round by round (SCHED_FLAG_PER_ROUND)."""
     b = {"small": lambda: W.random_small(2000, 50, n_max=40, M_lo=10, M_hi=80, a_max=30),
          "long": lambda: _long_batch(300, 51),
          "c4": lambda: W.c4(32, 52)}[shape]()
     b = W.with_prediction_noise(b, eps, seed=53)
-    for alpha in ((1, 10), (0, 1)):
-        o, g = check(K, ctx, oracle_mod, b, 4, f"protected eps={eps} alpha={alpha}", alpha=alpha)
+    for alpha in ((1, 10), (0, 1), (3, 10)):
+        o, g = check(K, ctx, oracle_mod, b, 4, f"protected eps={eps} alpha={alpha}", alpha=alpha,
+                     flags=flags)
     if shape == "small":
         assert o["evictions"].sum() > 0
 
