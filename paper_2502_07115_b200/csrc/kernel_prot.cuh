@@ -11,7 +11,8 @@
 // A request that completes before its predicted end (o < o~) leaves S at c = p + o; the
 // unused tail of its projection is removed then.  Such requests are chained per completion
 // round (bucket head per ring slot in shared memory, links in global scratch).
-// Rounds are processed one at a time (idle rounds are jumped).
+// Rounds are processed one at a time, except idle rounds and runs of quiet rounds (blocked
+// head, no overflow, no early completion), which are jumped up to 32 at a time.
 #pragma once
 #include "kernel_ring.cuh"
 
