@@ -379,6 +379,20 @@ def main():
         ab = {"per_round_kernel": ctx.last_kernel(), "per_round_ms_per_step": ab_ms,
               "per_round_value": rounds_rank * world / (ab_ms / 1000.0),
               "speedup_of_default": ab_ms / (ms_max / args.steps)}
+        # one warp per instance (k_mc_small for every instance) vs the default lane kernel
+        pw = K.Policy(pol.kind, pol.alpha, pol.beta_thresh, pol.seed, pol.round_cap,
+                      K.kvsched.FLAG_WARP_PER_INSTANCE)
+        ctx.run(off, req, mem, pw, out, id0=id0, hints=hints)
+        torch.cuda.synchronize(dev)
+        g0.record(stream)
+        for _ in range(args.steps):
+            ctx.run(off, req, mem, pw, out, id0=id0, hints=hints)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        wp_ms = g0.elapsed_time(g1) / args.steps
+        ab.update(warp_kernel=ctx.last_kernel(), warp_ms_per_step=wp_ms,
+                  warp_value=rounds_rank * world / (wp_ms / 1000.0),
+                  speedup_over_warp=wp_ms / (ms_max / args.steps))
 
     # configs[1] (C2, AM1: 10^4 instances of 1000 requests at t=0, M=40) under the same
     # protocol, reported beside the primary workload

@@ -1,0 +1,395 @@
+// kernel_lane.cuh -- MC-SF / MC-Benchmark with ONE LANE PER INSTANCE (the C5 bench path).
+//
+// k_mc_small spends a warp on one instance: 32 lanes evaluate Eq. 5 at 64 profile
+// positions in parallel, but every control step (queue pop, head decode, loop tests) is
+// executed by all 32 lanes for that one instance.  For small budgets (M <= 64) the whole
+// projected profile fits in 64 bytes, so here each lane runs its own instance and holds
+// its profile in 16 registers, four rounds per register (SWAR bytes):
+//
+//   byte tau-1 of P[0..15] = Prof(t + tau), tau = 1..64   (Eq. 5 LHS for the in-flight S)
+//
+// Eq. 5 for the head (s, w):  Prof(t+tau) + s + tau <= M  for tau in [1, w].
+// With G = Prof + tau <= M + 63 <= 127 one 32-bit add per word evaluates four rounds:
+//   y = P[i] + tau_i + (127 - (M - s))      -> bit 7 of a byte set  <=>  G > M - s
+//   m =        tau_i + (127 - w)            -> bit 7 of a byte set  <=>  tau > w
+// and the head fits iff no byte has bit 7 of (y & ~m) set (no byte ever carries: every
+// sum stays below 256).  Admission (Eq. 3) adds the ramp s + tau on tau <= w; the
+// clock advances by a one-byte funnel shift.  Rounds are stepped one at a time (no
+// look-ahead); the 32 lanes of a warp step 32 instances in lock step.
+//
+// Waiting queue R^(t): a 128-bit rank bitmap in four registers (rank = position in
+// (o~, idx) order for MC-SF; idx for MC-Benchmark).  Per-request words live
+// in shared memory, column `lane` of a [128][32] u32 array (bank = lane: conflict-free):
+//   low half  at position = rank : key {w:6 | s:3 | idx:7}
+//   high half at position = idx  : {rank:7 | a_(idx+1) - a_idx : 9}
+// Instances are claimed one lane at a time from the persistent work counter; the warp
+// stages a claimed instance cooperatively (coalesced 16-byte row loads, stable counting
+// sort on o~ for the MC-SF ranks) into the idle lane's column.
+//
+// Scope (checked per instance while staging): 1 <= n <= 128, M <= 64, 1 <= s <= 7,
+// o~ = o for MC-SF, s + o <= M, arrivals sorted with gaps <= 511, and no user round cap
+// (default cap: MC rounds never exceed max_a + sum o, so the cap is never reached).
+// Every other instance -- including invalid ones, whose status the general kernel
+// assigns -- is appended to a list that k_mc_small then runs.  Outputs are identical to
+// k_mc_small's (and the oracle's) field by field.
+#pragma once
+#include "params.cuh"
+
+namespace kv {
+
+constexpr int LANE_NP = 128;                 // requests per instance on the lane path
+constexpr int LANE_NW = 16;                  // profile words (bytes tau = 1..64)
+constexpr int LANE_WARP_BYTES = LANE_NP * 32 * 4 + 2048 + 64 * 4;   // words, F bytes, hist
+
+__device__ __forceinline__ uint32_t rep4(int x) { return (uint32_t)x * 0x01010101u; }
+__host__ __device__ constexpr uint32_t tau_word(int i)
+{
+    return (uint32_t)(4 * i + 1) | ((uint32_t)(4 * i + 2) << 8) | ((uint32_t)(4 * i + 3) << 16) |
+           ((uint32_t)(4 * i + 4) << 24);
+}
+// 0xFF in every byte whose bit 7 is set, 0x00 elsewhere (prmt sign replication)
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t m)
+{
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(m));
+    return r;
+}
+
+struct LaneInst {                            // one lane's instance (registers)
+    uint32_t P[LANE_NW];
+    uint32_t q0, q1, q2, q3;                 // waiting queue bitmap over ranks
+    long long inst, off, sumc, suma;
+    int t, a_next, next, n, M, h, s, w, hidx;
+    int maxc, peak, dr, nr;
+    bool active, dec, hstale;
+};
+
+// -------------------------------------------------------------------------------------
+// Stage instances into the idle lanes of `idle` (warp-uniform).  Returns false once the
+// work counter is exhausted.
+template <int POL>
+__device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, int *hist, LaneInst &L,
+                                            uint32_t idle)
+{
+    const int lane = lane_id();
+    uint16_t *d16 = reinterpret_cast<uint16_t *>(data);
+    while (idle) {
+        const int tl = __ffs(idle) - 1;
+        long long inst = 0;
+        if (lane == 0) inst = (long long)atomicAdd(P.counter, 1ull);
+        inst = __shfl_sync(KV_FULL, inst, 0);
+        if (inst >= P.n_inst) return false;
+        const long long off = P.offset[inst] - P.row_base;
+        const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
+        const int M = P.mem[inst];
+        bool ok = n >= 1 && n <= LANE_NP && M <= 64;
+        int4 r[4];
+        int an[4];
+        long long suma = 0;
+        if (ok) {
+            bool bad = false;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = lane + 32 * c;
+                r[c] = k < n ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = lane + 32 * c;
+                int nx = __shfl_down_sync(KV_FULL, r[c].x, 1);
+                const int nx0 = __shfl_sync(KV_FULL, r[c < 3 ? c + 1 : 3].x, 0);
+                if (lane == 31) nx = nx0;
+                an[c] = (k + 1 < n) ? nx - r[c].x : 0;           // a_(k+1) - a_k
+                if (k < n) {
+                    bad |= r[c].x < 0 || r[c].y < 1 || r[c].y > 7 || r[c].z < 1 || r[c].y + r[c].z > M;
+                    if (POL == POL_MCSF) bad |= r[c].w != r[c].z;
+                    bad |= an[c] < 0 || an[c] > 511;
+                    suma += r[c].x;
+                }
+            }
+            ok = !__any_sync(KV_FULL, bad);
+        }
+        if (!ok) {
+            if (lane == 0) {
+                const unsigned long long slot = atomicAdd(P.retry_count, 1ull);
+                P.retry_list[slot] = inst;
+            }
+            continue;
+        }
+        suma = warp_sum_i64(suma);
+        const int a0 = __shfl_sync(KV_FULL, r[0].x, 0);
+        // ranks: (o~, idx) order by a stable counting sort on o~ (MC-SF); idx (MC-Benchmark)
+        int rank[4];
+        if (POL == POL_MCSF) {
+            hist[lane] = 0;
+            hist[lane + 32] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = lane + 32 * c;
+                const int v = k < n ? r[c].z : 64 + lane;
+                const unsigned peers = __match_any_sync(KV_FULL, v);
+                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                __syncwarp();
+            }
+            const int h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+            int x = h0 + h1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(KV_FULL, x, d);
+                if (lane >= d) x += y;
+            }
+            __syncwarp();
+            hist[2 * lane] = x - h0 - h1;
+            hist[2 * lane + 1] = x - h1;
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int k = lane + 32 * c;
+                const int v = k < n ? r[c].z : 64 + lane;
+                const unsigned peers = __match_any_sync(KV_FULL, v);
+                rank[c] = k < n ? hist[v] + __popc(peers & ((1u << lane) - 1u)) : 0;
+                __syncwarp();
+                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                __syncwarp();
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rank[c] = lane + 32 * c;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int k = lane + 32 * c;
+            if (k < n) {
+                const uint32_t key = (uint32_t)r[c].z | ((uint32_t)r[c].y << 6) | ((uint32_t)k << 9);
+                d16[(rank[c] * 32 + tl) * 2] = (uint16_t)key;
+                d16[(k * 32 + tl) * 2 + 1] = (uint16_t)(rank[c] | (an[c] << 7));
+            }
+        }
+        __syncwarp();
+        if (lane == tl) {
+#pragma unroll
+            for (int i = 0; i < LANE_NW; ++i) L.P[i] = 0u;
+            L.q0 = L.q1 = L.q2 = L.q3 = 0u;
+            L.inst = inst;
+            L.off = off;
+            L.sumc = 0;
+            L.suma = suma;
+            L.t = a0;
+            L.a_next = a0;
+            L.next = 0;
+            L.n = n;
+            L.M = M;
+            L.h = KV_INF;
+            L.s = L.w = L.hidx = 0;
+            L.maxc = -1;
+            L.peak = 0;
+            L.dr = L.nr = 0;
+            L.active = true;
+            L.dec = false;
+            L.hstale = false;
+        }
+        idle &= idle - 1;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void lane_write_result(const KParams &P, const LaneInst &L)
+{
+    if (P.tel) P.tel[L.inst] = L.sumc - L.suma;
+    if (P.rounds) P.rounds[L.inst] = (long long)(L.dr + L.nr);
+    if (P.drounds) P.drounds[L.inst] = (long long)L.dr;
+    if (P.evictions) P.evictions[L.inst] = 0;
+    if (P.makespan) P.makespan[L.inst] = L.maxc;
+    if (P.peak) P.peak[L.inst] = L.peak;
+    if (P.status) P.status[L.inst] = ST_OK;
+}
+
+// max over the 64 profile bytes, as 16x2 halves (values <= 64)
+__device__ __forceinline__ uint32_t max_bytes16(const uint32_t (&P)[LANE_NW], uint32_t acc)
+{
+#pragma unroll
+    for (int i = 0; i < LANE_NW; ++i)
+        acc = __vimax3_s16x2_relu(acc, __byte_perm(P[i], 0u, 0x4240), __byte_perm(P[i], 0u, 0x4341));
+    return acc;
+}
+
+// P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau); d >= 63 clears it
+// (byte 63, tau = 64, is always zero: no window reaches past t + 63)
+__device__ __forceinline__ void shift_bytes(uint32_t (&P)[LANE_NW], int d)
+{
+    d = min(d, 63);
+    const int q = d >> 2;
+#pragma unroll
+    for (int b = 8; b >= 1; b >>= 1) {
+        const bool on = (q & b) != 0;
+#pragma unroll
+        for (int i = 0; i < LANE_NW; ++i) P[i] = on ? (i + b < LANE_NW ? P[i + b] : 0u) : P[i];
+    }
+    const int sh = (d & 3) * 8;
+#pragma unroll
+    for (int i = 0; i < LANE_NW - 1; ++i) P[i] = __funnelshift_r(P[i], P[i + 1], sh);
+    P[LANE_NW - 1] >>= sh;
+}
+
+// -------------------------------------------------------------------------------------
+// First round offset D >= 0 at which the head (s, w) satisfies Eq. 5 while the profile
+// only advances (no admission, arrival or early completion in between).  Position u
+// (relative to t) blocks exactly the offsets D in [u - w, c_u - 1] with
+//     c_u = max(0, min(u, Prof(t+u) + u - (M - s)))
+// (for D < u, u lies in the window [D+1, D+w] iff D >= u - w, and fails iff
+// Prof(t+u) + s + u - D > M).  So D is feasible iff every u <= D + w has c_u <= D, i.e.
+//     feasible(D)  <=>  F(D + w) <= D,       F(x) = max_{u <= x} c_u,
+// and D* is the least fixpoint of D <- F(D + w) from D = 0 (F is non-decreasing, so every
+// D skipped by that iteration is infeasible).  Positions past 64 hold no projection
+// (c_u = u - (M-s) <= D there), so F(x) = F(min(x, 64)).
+// c and F are computed four rounds at a time in 16x2 halves (DPX VIADDMNMX / VIMNMX),
+// F is packed to bytes in the lane's shared-memory column, and the fixpoint walks it.
+// The same pass folds every profile byte into pk16 (peak memory, see k_mc_lane).
+__device__ __forceinline__ int first_fit(const uint32_t (&P)[LANE_NW], int L, int w, unsigned char *fcol,
+                                         uint32_t &pk16)
+{
+    const uint32_t mL = (uint32_t)(-L) & 0xffffu;
+    const uint32_t nL2 = mL | (mL << 16);                     // -L in both halves
+    uint32_t run = 0u;                                        // F of the previous word, both halves
+    uint32_t fw[LANE_NW];
+#pragma unroll
+    for (int i = 0; i < LANE_NW; ++i) {
+        const uint32_t xe = __byte_perm(P[i], 0u, 0x4240);    // Prof at tau = 4i+1, 4i+3
+        const uint32_t xo = __byte_perm(P[i], 0u, 0x4341);    // Prof at tau = 4i+2, 4i+4
+        pk16 = __vimax3_s16x2_relu(pk16, xe, xo);
+        const uint32_t te = (uint32_t)(4 * i + 1) | ((uint32_t)(4 * i + 3) << 16);
+        const uint32_t to = (uint32_t)(4 * i + 2) | ((uint32_t)(4 * i + 4) << 16);
+        // c = max(0, min(tau, Prof + tau - L)) = max(0, min(min(Prof - L, 0) + tau, tau))
+        const uint32_t ce = __viaddmin_s16x2_relu(__viaddmin_s16x2(xe, nL2, 0u), te, te);
+        const uint32_t co = __viaddmin_s16x2_relu(__viaddmin_s16x2(xo, nL2, 0u), to, to);
+        // prefix maximum over tau = 4i+1, 4i+2, 4i+3, 4i+4
+        const uint32_t t1 = __vimax3_s16x2_relu(ce, co, run);  // lo = F(4i+2), hi = max(run, c3, c4)
+        const uint32_t po = __vimax_s16x2_relu(t1, __byte_perm(t1, 0u, 0x1010));   // (F2, F4)
+        const uint32_t pe = __vimax_s16x2_relu(ce, __byte_perm(run, po, 0x5410));  // (F1, F3)
+        run = __byte_perm(po, 0u, 0x3232);
+        fw[i] = __byte_perm(pe, po, 0x6240);                  // bytes F(4i+1) .. F(4i+4)
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4 *>(fcol + c * 512) = make_uint4(fw[4 * c], fw[4 * c + 1], fw[4 * c + 2], fw[4 * c + 3]);
+    int D = 0;
+    for (;;) {
+        const int x = min(D + w, 64) - 1;
+        const int f = fcol[(x >> 4) * 512 + (x & 15)];
+        if (f <= D) break;
+        D = f;
+    }
+    return D;
+}
+
+__device__ __forceinline__ int hmax16(uint32_t v) { return max((int)(v & 0xffffu), (int)(v >> 16)); }
+
+// -------------------------------------------------------------------------------------
+template <int POL>
+__global__ void __launch_bounds__(128, 3) k_mc_lane(const KParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *wbase = smem_raw + (size_t)warp * LANE_WARP_BYTES;
+    uint32_t *data = reinterpret_cast<uint32_t *>(wbase);
+    unsigned char *fcol = wbase + LANE_NP * 32 * 4 + lane * 16;   // F bytes: [4][32 lanes][16]
+    int *hist = reinterpret_cast<int *>(wbase + LANE_NP * 32 * 4 + 2048);
+    const uint32_t *col = data + lane;           // this lane's column: word k at col[32 k]
+
+    LaneInst L;
+    L.active = false;
+    uint32_t pk16 = 0u;
+    bool more = true;
+    for (;;) {
+        const uint32_t idle = __ballot_sync(KV_FULL, !L.active);
+        if (idle && more) {
+            more = lane_refill<POL>(P, data, hist, L, idle);
+            if (idle & (1u << lane)) pk16 = 0u;
+        }
+        if (!__any_sync(KV_FULL, L.active)) break;
+        if (!L.active) continue;
+
+        // arrivals a_i <= t join R^(t)
+        while (L.a_next <= L.t) {
+            const uint32_t d = col[32 * L.next] >> 16;
+            const int r = (int)(d & 127u);
+            const uint32_t bit = 1u << (r & 31);
+            const int wq = r >> 5;
+            L.q0 |= wq == 0 ? bit : 0u;
+            L.q1 |= wq == 1 ? bit : 0u;
+            L.q2 |= wq == 2 ? bit : 0u;
+            L.q3 |= wq == 3 ? bit : 0u;
+            if (r < L.h) { L.h = r; L.hstale = true; }
+            L.a_next = (++L.next < L.n) ? L.a_next + (int)(d >> 7) : KV_INF;
+        }
+
+        int jump = 0;
+        if (L.h == KV_INF) {
+            // R empty: every projected byte is final (no admission can add to it); fold
+            // them into the peak before they are shifted out
+            pk16 = max_bytes16(L.P, pk16);
+            if (L.next == L.n) {                         // R and arrivals exhausted: drain S
+                if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
+                else L.nr += max(0, L.maxc - L.t);
+                L.peak = max(L.peak, hmax16(pk16));
+                lane_write_result(P, L);
+                L.active = false;
+                continue;
+            }
+            // rounds t .. a_next-1: S only (non-idle while t < maxc), no decision
+            const int tn = L.a_next;
+            if (L.dec) { ++L.dr; L.nr += max(0, min(tn, L.maxc) - L.t - 1); }
+            else L.nr += max(0, min(tn, L.maxc) - L.t);
+            jump = tn - L.t;
+        } else {
+            if (L.hstale) {
+                const uint32_t key = col[32 * L.h] & 0xffffu;
+                L.w = (int)(key & 63u);
+                L.s = (int)((key >> 6) & 7u);
+                L.hidx = (int)(key >> 9);
+                L.hstale = false;
+            }
+            // Eq. 5 for the head at this round and, if it fails, the first round it holds
+            const int D = first_fit(L.P, L.M - L.s, L.w, fcol, pk16);
+            if (D == 0) {                                      // admit: p = t, c = t + o
+                L.dec = true;
+                const uint32_t S4 = rep4(L.s);
+                const uint32_t Kw = rep4(127 - L.w);
+#pragma unroll
+                for (int i = 0; i < LANE_NW; ++i)
+                    L.P[i] += (S4 + tau_word(i)) & ~sign_bytes(Kw + tau_word(i));
+                const int c = L.t + L.w;
+                if (P.start) P.start[L.off + L.hidx] = L.t;
+                if (P.completion) P.completion[L.off + L.hidx] = c;
+                L.sumc += c;
+                L.maxc = max(L.maxc, c);
+                const int h = L.h;
+                const uint32_t nb = ~(1u << (h & 31));
+                const int wq = h >> 5;
+                L.q0 &= wq == 0 ? nb : ~0u;
+                L.q1 &= wq == 1 ? nb : ~0u;
+                L.q2 &= wq == 2 ? nb : ~0u;
+                L.q3 &= wq == 3 ? nb : ~0u;
+                L.h = L.q0 ? __ffs(L.q0) - 1
+                    : L.q1 ? 31 + __ffs(L.q1)
+                    : L.q2 ? 63 + __ffs(L.q2)
+                    : L.q3 ? 95 + __ffs(L.q3) : KV_INF;
+                L.hstale = true;
+            } else {
+                // rounds t .. t+D-1 are decision rounds that admit nothing.  MC-SF: an
+                // arrival may sort before the head, so stop at the next arrival (it joins
+                // R there); MC-Benchmark: arrivals queue behind the head.
+                jump = (POL == POL_MCSF) ? min(D, L.a_next - L.t) : D;
+                L.dr += jump;
+            }
+        }
+        if (jump > 0) {
+            shift_bytes(L.P, jump);
+            L.t += jump;
+            L.dec = false;
+        }
+    }
+}
+
+}  // namespace kv

@@ -486,15 +486,18 @@ __global__ void __launch_bounds__(128, KV_SMALL_MIN_BLOCKS) k_mc_small(const KPa
     S.sm = reinterpret_cast<uint32_t *>(base + NP * 18 + (NP / 32) * 4);
     S.hist = reinterpret_cast<int *>(base + NP * 18 + (NP / 32) * 4 + 128);
 
-    long long inst = 0;
-    if (lane == 0) inst = atomicAdd(P.counter, 1ull);
-    inst = __shfl_sync(KV_FULL, inst, 0);
-    while (inst < P.n_inst) {
+    // work item w is instance w, or work_list[w] for the instances k_mc_lane handed over
+    const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+    long long w = 0;
+    if (lane == 0) w = atomicAdd(P.counter, 1ull);
+    w = __shfl_sync(KV_FULL, w, 0);
+    while (w < n_work) {
         long long nxt = 0;     // claim the next instance now; the latency hides behind this one
         if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
+        const long long inst = P.work_list ? P.work_list[w] : w;
         if (QREG) small_instance<POL, MULTI, RegQueue>(P, inst, S);
         else small_instance<POL, MULTI, SmemQueue>(P, inst, S);
-        inst = __shfl_sync(KV_FULL, nxt, 0);
+        w = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();
     }
 }

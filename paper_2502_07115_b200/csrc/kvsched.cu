@@ -18,6 +18,7 @@
 #include "kernel_prot.cuh"
 #include "kernel_ring.cuh"
 #include "kernel_small.cuh"
+#include "kernel_lane.cuh"
 
 using namespace kv;
 
@@ -258,6 +259,33 @@ int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const c
     return SCHED_OK;
 }
 
+// one-lane-per-instance kernel: 4 warps per block, a persistent grid of full occupancy
+template <typename K>
+int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
+{
+    const int block = 128, smem = 4 * LANE_WARP_BYTES;
+    CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int grid = 1;
+    int rc = occupancy_grid(c, kernel, block, smem, (P.n_inst + 31) / 32, &grid);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    }
+    kernel<<<grid, block, smem, c->stream>>>(P);
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->timing) {
+        CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+        c->pending.emplace_back(e0, e1);
+    }
+    c->launches++;
+    c->sim_launches++;
+    c->last_kernel = name;
+    return SCHED_OK;
+}
+
 int check_common(sched_ctx *c, const sched_instances *inst)
 {
     if (!c) return SCHED_E_STATE;
@@ -281,7 +309,8 @@ int check_policy(sched_ctx *c, const sched_policy *pol)
     if (!pol) return fail(c, SCHED_E_ARG, "pol is NULL");
     if (pol->policy < SCHED_MCSF || pol->policy > SCHED_MCSF_PROTECTED)
         return fail(c, SCHED_E_ARG, "unknown policy %d", pol->policy);
-    if (pol->flags & ~SCHED_FLAG_PER_ROUND) return fail(c, SCHED_E_ARG, "unknown flags 0x%x", pol->flags);
+    if (pol->flags & ~(SCHED_FLAG_PER_ROUND | SCHED_FLAG_WARP_PER_INSTANCE))
+        return fail(c, SCHED_E_ARG, "unknown flags 0x%x", pol->flags);
     if (pol->policy >= SCHED_ALPHA) {
         if (pol->alpha_den <= 0 || pol->alpha_num < 0 || pol->alpha_num >= pol->alpha_den)
             return fail(c, SCHED_E_ARG, "alpha = %d/%d must lie in [0, 1)", pol->alpha_num, pol->alpha_den);
@@ -411,6 +440,23 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         const int smem = P.warp_bytes;
         const bool per_round = pol->flags & SCHED_FLAG_PER_ROUND;
         const bool qreg = P.NP <= 1024;          // waiting queue fits one word per lane
+        if (!per_round && !(pol->flags & SCHED_FLAG_WARP_PER_INSTANCE) && pol->round_cap <= 0 &&
+            (size_t)LANE_WARP_BYTES * 4 <= c->max_smem_optin) {
+            // one lane per instance; instances outside its scope are listed for k_mc_small
+            if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
+            P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
+            P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
+            CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
+            const char *lname = pol->policy == SCHED_MCSF ? "k_mc_lane<MCSF>" : "k_mc_lane<MCBENCH>";
+            rc = pol->policy == SCHED_MCSF ? launch_lane(c, k_mc_lane<POL_MCSF>, P, lname)
+                                           : launch_lane(c, k_mc_lane<POL_MCBENCH>, P, lname);
+            if (rc) return rc;
+            P.work_list = P.retry_list;
+            P.work_count = P.retry_count;
+            P.retry_list = nullptr;
+            P.retry_count = nullptr;
+            CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+        }
 #define KV_SMALL(POLV, MULTIV, QREGV, NAME) launch_sim(c, k_mc_small<POLV, MULTIV, QREGV>, P, smem, NAME)
         if (pol->policy == SCHED_MCSF) {
             if (per_round) return qreg ? KV_SMALL(POL_MCSF, false, true, "k_mc_small<MCSF,per-round>")

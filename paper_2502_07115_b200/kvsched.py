@@ -20,6 +20,7 @@ POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": A
               "mcsf_protected": MCSF_PROTECTED}
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
+FLAG_WARP_PER_INSTANCE = 2
 REQ_I32X4, REQ_U16X4_DELTA = 0, 1
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}
 
