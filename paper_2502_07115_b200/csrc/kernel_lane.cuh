@@ -55,8 +55,9 @@ __device__ __forceinline__ uint32_t sign_bytes(uint32_t m)
     return r;
 }
 
+template <int NW>
 struct LaneInst {                            // one lane's instance (registers)
-    uint32_t P[LANE_NW];
+    uint32_t P[NW];
     uint32_t q0, q1, q2, q3;                 // waiting queue bitmap over ranks
     long long inst, off, sumc, suma;
     int t, a_next, next, n, M, h, s, w, hidx;
@@ -67,8 +68,8 @@ struct LaneInst {                            // one lane's instance (registers)
 // -------------------------------------------------------------------------------------
 // Stage instances into the idle lanes of `idle` (warp-uniform).  Returns false once the
 // work counter is exhausted.
-template <int POL>
-__device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, int *hist, LaneInst &L,
+template <int POL, int NW>
+__device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, int *hist, LaneInst<NW> &L,
                                             uint32_t idle)
 {
     const int lane = lane_id();
@@ -101,7 +102,8 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
                 if (lane == 31) nx = nx0;
                 an[c] = (k + 1 < n) ? nx - r[c].x : 0;           // a_(k+1) - a_k
                 if (k < n) {
-                    bad |= r[c].x < 0 || r[c].y < 1 || r[c].y > 7 || r[c].z < 1 || r[c].y + r[c].z > M;
+                    bad |= r[c].x < 0 || r[c].y < 1 || r[c].y > 7 || r[c].z < 1 || r[c].y + r[c].z > M ||
+                           r[c].z >= 4 * NW;               // window within the profile words
                     if (POL == POL_MCSF) bad |= r[c].w != r[c].z;
                     bad |= an[c] < 0 || an[c] > 511;
                     suma += r[c].x;
@@ -169,7 +171,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         __syncwarp();
         if (lane == tl) {
 #pragma unroll
-            for (int i = 0; i < LANE_NW; ++i) L.P[i] = 0u;
+            for (int i = 0; i < NW; ++i) L.P[i] = 0u;
             L.q0 = L.q1 = L.q2 = L.q3 = 0u;
             L.inst = inst;
             L.off = off;
@@ -194,7 +196,8 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
     return true;
 }
 
-__device__ __forceinline__ void lane_write_result(const KParams &P, const LaneInst &L)
+template <int NW>
+__device__ __forceinline__ void lane_write_result(const KParams &P, const LaneInst<NW> &L)
 {
     if (P.tel) P.tel[L.inst] = L.sumc - L.suma;
     if (P.rounds) P.rounds[L.inst] = (long long)(L.dr + L.nr);
@@ -205,31 +208,48 @@ __device__ __forceinline__ void lane_write_result(const KParams &P, const LaneIn
     if (P.status) P.status[L.inst] = ST_OK;
 }
 
-// max over the 64 profile bytes, as 16x2 halves (values <= 64)
-__device__ __forceinline__ uint32_t max_bytes16(const uint32_t (&P)[LANE_NW], uint32_t acc)
+// max over the profile bytes, as 16x2 halves (values <= 64)
+template <int NW>
+__device__ __forceinline__ uint32_t max_bytes16(const uint32_t (&P)[NW], uint32_t acc)
 {
 #pragma unroll
-    for (int i = 0; i < LANE_NW; ++i)
+    for (int i = 0; i < NW; ++i)
         acc = __vimax3_s16x2_relu(acc, __byte_perm(P[i], 0u, 0x4240), __byte_perm(P[i], 0u, 0x4341));
     return acc;
 }
 
-// P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau); d >= 63 clears it
-// (byte 63, tau = 64, is always zero: no window reaches past t + 63)
-__device__ __forceinline__ void shift_bytes(uint32_t (&P)[LANE_NW], int d)
+// P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau).  Byte 4 NW - 1 is
+// always zero (every window ends before it), so d >= 4 NW - 1 clears the profile.  The
+// word stages are predicated moves (FMA pipe), skipped by the whole warp when no lane
+// needs them.
+template <int NW>
+__device__ __forceinline__ void shift_bytes(uint32_t (&P)[NW], int d)
 {
-    d = min(d, 63);
+    d = min(d, 4 * NW - 1);
     const int q = d >> 2;
 #pragma unroll
     for (int b = 8; b >= 1; b >>= 1) {
+        if (b >= NW) continue;
         const bool on = (q & b) != 0;
+        if (__any_sync(KV_FULL, on)) {
 #pragma unroll
-        for (int i = 0; i < LANE_NW; ++i) P[i] = on ? (i + b < LANE_NW ? P[i + b] : 0u) : P[i];
+            for (int i = 0; i < NW; ++i)
+                if (on) P[i] = i + b < NW ? P[i + b] : 0u;
+        }
     }
     const int sh = (d & 3) * 8;
 #pragma unroll
-    for (int i = 0; i < LANE_NW - 1; ++i) P[i] = __funnelshift_r(P[i], P[i + 1], sh);
-    P[LANE_NW - 1] >>= sh;
+    for (int i = 0; i < NW - 1; ++i) P[i] = __funnelshift_r(P[i], P[i + 1], sh);
+    P[NW - 1] >>= sh;
+}
+
+// x + y on the FMA pipe (IMAD), leaving the ALU pipe -- the kernel's binding resource --
+// to the SWAR / DPX work
+__device__ __forceinline__ uint32_t add_fma(uint32_t x, uint32_t y)
+{
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return r;
 }
 
 // -------------------------------------------------------------------------------------
@@ -246,37 +266,43 @@ __device__ __forceinline__ void shift_bytes(uint32_t (&P)[LANE_NW], int d)
 // c and F are computed four rounds at a time in 16x2 halves (DPX VIADDMNMX / VIMNMX),
 // F is packed to bytes in the lane's shared-memory column, and the fixpoint walks it.
 // The same pass folds every profile byte into pk16 (peak memory, see k_mc_lane).
-__device__ __forceinline__ int first_fit(const uint32_t (&P)[LANE_NW], int L, int w, unsigned char *fcol,
+template <int NW>
+__device__ __forceinline__ int first_fit(const uint32_t (&P)[NW], int L, int w, unsigned char *fcol,
                                          uint32_t &pk16)
 {
-    const uint32_t mL = (uint32_t)(-L) & 0xffffu;
-    const uint32_t nL2 = mL | (mL << 16);                     // -L in both halves
-    uint32_t run = 0u;                                        // F of the previous word, both halves
-    uint32_t fw[LANE_NW];
+    // every 16-bit value below carries a bias of 64 so that it stays positive and plain
+    // 32-bit adds (FMA pipe) never carry between the halves
+    const uint32_t b64 = 0x00400040u;
+    const uint32_t kL = (uint32_t)(64 - L) * 0x00010001u;     // 64 - L in both halves (>= 1)
+    uint32_t run = b64;                                       // F of the previous word, both halves
+    uint32_t fw[16];
 #pragma unroll
-    for (int i = 0; i < LANE_NW; ++i) {
+    for (int i = 0; i < NW; ++i) {
         const uint32_t xe = __byte_perm(P[i], 0u, 0x4240);    // Prof at tau = 4i+1, 4i+3
         const uint32_t xo = __byte_perm(P[i], 0u, 0x4341);    // Prof at tau = 4i+2, 4i+4
         pk16 = __vimax3_s16x2_relu(pk16, xe, xo);
         const uint32_t te = (uint32_t)(4 * i + 1) | ((uint32_t)(4 * i + 3) << 16);
         const uint32_t to = (uint32_t)(4 * i + 2) | ((uint32_t)(4 * i + 4) << 16);
-        // c = max(0, min(tau, Prof + tau - L)) = max(0, min(min(Prof - L, 0) + tau, tau))
-        const uint32_t ce = __viaddmin_s16x2_relu(__viaddmin_s16x2(xe, nL2, 0u), te, te);
-        const uint32_t co = __viaddmin_s16x2_relu(__viaddmin_s16x2(xo, nL2, 0u), to, to);
+        // 64 + c' with c' = min(Prof - L, 0) + tau = min(tau, Prof + tau - L) in [-62, 64];
+        // c = max(c', 0) comes from starting the running maximum at the bias
+        const uint32_t ce = add_fma(__viaddmin_s16x2(xe, kL, b64), te);
+        const uint32_t co = add_fma(__viaddmin_s16x2(xo, kL, b64), to);
         // prefix maximum over tau = 4i+1, 4i+2, 4i+3, 4i+4
         const uint32_t t1 = __vimax3_s16x2_relu(ce, co, run);  // lo = F(4i+2), hi = max(run, c3, c4)
         const uint32_t po = __vimax_s16x2_relu(t1, __byte_perm(t1, 0u, 0x1010));   // (F2, F4)
         const uint32_t pe = __vimax_s16x2_relu(ce, __byte_perm(run, po, 0x5410));  // (F1, F3)
         run = __byte_perm(po, 0u, 0x3232);
-        fw[i] = __byte_perm(pe, po, 0x6240);                  // bytes F(4i+1) .. F(4i+4)
+        fw[i] = __byte_perm(pe, po, 0x6240);                  // bytes 64 + F(4i+1) .. 64 + F(4i+4)
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int i = NW; i < 16; ++i) fw[i] = 0u;
+#pragma unroll
+    for (int c = 0; c < (NW + 3) / 4; ++c)
         *reinterpret_cast<uint4 *>(fcol + c * 512) = make_uint4(fw[4 * c], fw[4 * c + 1], fw[4 * c + 2], fw[4 * c + 3]);
     int D = 0;
     for (;;) {
-        const int x = min(D + w, 64) - 1;
-        const int f = fcol[(x >> 4) * 512 + (x & 15)];
+        const int x = min(D + w, 4 * NW) - 1;
+        const int f = (int)fcol[(x >> 4) * 512 + (x & 15)] - 64;
         if (f <= D) break;
         D = f;
     }
@@ -286,7 +312,7 @@ __device__ __forceinline__ int first_fit(const uint32_t (&P)[LANE_NW], int L, in
 __device__ __forceinline__ int hmax16(uint32_t v) { return max((int)(v & 0xffffu), (int)(v >> 16)); }
 
 // -------------------------------------------------------------------------------------
-template <int POL>
+template <int POL, int NW>
 __global__ void __launch_bounds__(128, 3) k_mc_lane(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -297,95 +323,100 @@ __global__ void __launch_bounds__(128, 3) k_mc_lane(const KParams P)
     int *hist = reinterpret_cast<int *>(wbase + LANE_NP * 32 * 4 + 2048);
     const uint32_t *col = data + lane;           // this lane's column: word k at col[32 k]
 
-    LaneInst L;
+    LaneInst<NW> L;
     L.active = false;
     uint32_t pk16 = 0u;
     bool more = true;
     for (;;) {
         const uint32_t idle = __ballot_sync(KV_FULL, !L.active);
         if (idle && more) {
-            more = lane_refill<POL>(P, data, hist, L, idle);
+            more = lane_refill<POL, NW>(P, data, hist, L, idle);
             if (idle & (1u << lane)) pk16 = 0u;
         }
         if (!__any_sync(KV_FULL, L.active)) break;
-        if (!L.active) continue;
 
-        // arrivals a_i <= t join R^(t)
-        while (L.a_next <= L.t) {
-            const uint32_t d = col[32 * L.next] >> 16;
-            const int r = (int)(d & 127u);
-            const uint32_t bit = 1u << (r & 31);
-            const int wq = r >> 5;
-            L.q0 |= wq == 0 ? bit : 0u;
-            L.q1 |= wq == 1 ? bit : 0u;
-            L.q2 |= wq == 2 ? bit : 0u;
-            L.q3 |= wq == 3 ? bit : 0u;
-            if (r < L.h) { L.h = r; L.hstale = true; }
-            L.a_next = (++L.next < L.n) ? L.a_next + (int)(d >> 7) : KV_INF;
-        }
-
+        // One step of this lane's instance.  No lane leaves the iteration early: the
+        // profile shift at the end votes across the warp.
         int jump = 0;
-        if (L.h == KV_INF) {
-            // R empty: every projected byte is final (no admission can add to it); fold
-            // them into the peak before they are shifted out
-            pk16 = max_bytes16(L.P, pk16);
-            if (L.next == L.n) {                         // R and arrivals exhausted: drain S
-                if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
-                else L.nr += max(0, L.maxc - L.t);
-                L.peak = max(L.peak, hmax16(pk16));
-                lane_write_result(P, L);
-                L.active = false;
-                continue;
+        if (L.active) {
+            // arrivals a_i <= t join R^(t)
+            while (L.a_next <= L.t) {
+                const uint32_t d = col[32 * L.next] >> 16;
+                const int r = (int)(d & 127u);
+                const uint32_t bit = 1u << (r & 31);
+                const int wq = r >> 5;
+                L.q0 |= wq == 0 ? bit : 0u;
+                L.q1 |= wq == 1 ? bit : 0u;
+                L.q2 |= wq == 2 ? bit : 0u;
+                L.q3 |= wq == 3 ? bit : 0u;
+                if (r < L.h) { L.h = r; L.hstale = true; }
+                L.a_next = (++L.next < L.n) ? L.a_next + (int)(d >> 7) : KV_INF;
             }
-            // rounds t .. a_next-1: S only (non-idle while t < maxc), no decision
-            const int tn = L.a_next;
-            if (L.dec) { ++L.dr; L.nr += max(0, min(tn, L.maxc) - L.t - 1); }
-            else L.nr += max(0, min(tn, L.maxc) - L.t);
-            jump = tn - L.t;
-        } else {
-            if (L.hstale) {
-                const uint32_t key = col[32 * L.h] & 0xffffu;
-                L.w = (int)(key & 63u);
-                L.s = (int)((key >> 6) & 7u);
-                L.hidx = (int)(key >> 9);
-                L.hstale = false;
-            }
-            // Eq. 5 for the head at this round and, if it fails, the first round it holds
-            const int D = first_fit(L.P, L.M - L.s, L.w, fcol, pk16);
-            if (D == 0) {                                      // admit: p = t, c = t + o
-                L.dec = true;
-                const uint32_t S4 = rep4(L.s);
-                const uint32_t Kw = rep4(127 - L.w);
-#pragma unroll
-                for (int i = 0; i < LANE_NW; ++i)
-                    L.P[i] += (S4 + tau_word(i)) & ~sign_bytes(Kw + tau_word(i));
-                const int c = L.t + L.w;
-                if (P.start) P.start[L.off + L.hidx] = L.t;
-                if (P.completion) P.completion[L.off + L.hidx] = c;
-                L.sumc += c;
-                L.maxc = max(L.maxc, c);
-                const int h = L.h;
-                const uint32_t nb = ~(1u << (h & 31));
-                const int wq = h >> 5;
-                L.q0 &= wq == 0 ? nb : ~0u;
-                L.q1 &= wq == 1 ? nb : ~0u;
-                L.q2 &= wq == 2 ? nb : ~0u;
-                L.q3 &= wq == 3 ? nb : ~0u;
-                L.h = L.q0 ? __ffs(L.q0) - 1
-                    : L.q1 ? 31 + __ffs(L.q1)
-                    : L.q2 ? 63 + __ffs(L.q2)
-                    : L.q3 ? 95 + __ffs(L.q3) : KV_INF;
-                L.hstale = true;
+
+            if (L.h == KV_INF) {
+                // R empty: every projected byte is final (no admission can add to it); fold
+                // them into the peak before they are shifted out
+                pk16 = max_bytes16(L.P, pk16);
+                if (L.next == L.n) {                         // R and arrivals exhausted: drain S
+                    if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
+                    else L.nr += max(0, L.maxc - L.t);
+                    L.peak = max(L.peak, hmax16(pk16));
+                    lane_write_result(P, L);
+                    L.active = false;
+                } else if (L.maxc <= L.t) {                  // S and R empty: idle until a_next
+                    L.t = L.a_next;                          // (the profile is all zero)
+                } else {
+                    // rounds t .. a_next-1: S only (non-idle while t < maxc), no decision
+                    const int tn = L.a_next;
+                    if (L.dec) { ++L.dr; L.nr += max(0, min(tn, L.maxc) - L.t - 1); }
+                    else L.nr += max(0, min(tn, L.maxc) - L.t);
+                    jump = tn - L.t;
+                }
             } else {
-                // rounds t .. t+D-1 are decision rounds that admit nothing.  MC-SF: an
-                // arrival may sort before the head, so stop at the next arrival (it joins
-                // R there); MC-Benchmark: arrivals queue behind the head.
-                jump = (POL == POL_MCSF) ? min(D, L.a_next - L.t) : D;
-                L.dr += jump;
+                if (L.hstale) {
+                    const uint32_t key = col[32 * L.h] & 0xffffu;
+                    L.w = (int)(key & 63u);
+                    L.s = (int)((key >> 6) & 7u);
+                    L.hidx = (int)(key >> 9);
+                    L.hstale = false;
+                }
+                // Eq. 5 for the head at this round and, if it fails, the first round it holds
+                const int D = first_fit(L.P, L.M - L.s, L.w, fcol, pk16);
+                if (D == 0) {                                      // admit: p = t, c = t + o
+                    L.dec = true;
+                    const uint32_t S4 = rep4(L.s);
+                    const uint32_t Kw = rep4(127 - L.w);
+#pragma unroll
+                    for (int i = 0; i < NW; ++i)
+                        L.P[i] = add_fma(L.P[i], add_fma(S4, tau_word(i)) & ~sign_bytes(Kw + tau_word(i)));
+                    const int c = L.t + L.w;
+                    if (P.start) P.start[L.off + L.hidx] = L.t;
+                    if (P.completion) P.completion[L.off + L.hidx] = c;
+                    L.sumc += c;
+                    L.maxc = max(L.maxc, c);
+                    const int h = L.h;
+                    const uint32_t nb = ~(1u << (h & 31));
+                    const int wq = h >> 5;
+                    L.q0 &= wq == 0 ? nb : ~0u;
+                    L.q1 &= wq == 1 ? nb : ~0u;
+                    L.q2 &= wq == 2 ? nb : ~0u;
+                    L.q3 &= wq == 3 ? nb : ~0u;
+                    L.h = L.q0 ? __ffs(L.q0) - 1
+                        : L.q1 ? 31 + __ffs(L.q1)
+                        : L.q2 ? 63 + __ffs(L.q2)
+                        : L.q3 ? 95 + __ffs(L.q3) : KV_INF;
+                    L.hstale = true;
+                } else {
+                    // rounds t .. t+D-1 are decision rounds that admit nothing.  MC-SF: an
+                    // arrival may sort before the head, so stop at the next arrival (it joins
+                    // R there); MC-Benchmark: arrivals queue behind the head.
+                    jump = (POL == POL_MCSF) ? min(D, L.a_next - L.t) : D;
+                    L.dr += jump;
+                }
             }
         }
+        shift_bytes(L.P, jump);                                // all 32 lanes (jump 0 = no-op)
         if (jump > 0) {
-            shift_bytes(L.P, jump);
             L.t += jump;
             L.dec = false;
         }

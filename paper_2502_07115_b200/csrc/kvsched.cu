@@ -447,9 +447,13 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
             P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
             CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
-            const char *lname = pol->policy == SCHED_MCSF ? "k_mc_lane<MCSF>" : "k_mc_lane<MCBENCH>";
-            rc = pol->policy == SCHED_MCSF ? launch_lane(c, k_mc_lane<POL_MCSF>, P, lname)
-                                           : launch_lane(c, k_mc_lane<POL_MCBENCH>, P, lname);
+            // profile words: bytes tau = 1 .. 4 NW with byte 4 NW - 1 never reached by a window
+            const int nw = max_len < 16 ? 4 : max_len < 32 ? 8 : max_len < 52 ? 13 : 16;
+            const bool sf = pol->policy == SCHED_MCSF;
+#define KV_LANE(NWV) (sf ? launch_lane(c, k_mc_lane<POL_MCSF, NWV>, P, "k_mc_lane<MCSF>")                 \
+                         : launch_lane(c, k_mc_lane<POL_MCBENCH, NWV>, P, "k_mc_lane<MCBENCH>"))
+            rc = nw == 4 ? KV_LANE(4) : nw == 8 ? KV_LANE(8) : nw == 13 ? KV_LANE(13) : KV_LANE(16);
+#undef KV_LANE
             if (rc) return rc;
             P.work_list = P.retry_list;
             P.work_count = P.retry_count;
