@@ -83,7 +83,8 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
         const int M = P.mem[inst];
-        bool ok = n >= 1 && n <= LANE_NP && M <= 64;
+        // in scope, and within the caller's size hints (k_mc_small reports violations)
+        bool ok = n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
         int4 r[4];
         int an[4];
         long long suma = 0;

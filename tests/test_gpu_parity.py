@@ -129,6 +129,46 @@ def test_per_round_and_multi_round_modes(K, ctx, oracle_mod, maker, pol):
         check(K, ctx, oracle_mod, b, pol, f"{maker} flags={flags}", flags=flags, **kw)
 
 
+def _concat(*batches):
+    insts = []
+    for b in batches:
+        insts += [b.instance(k) for k in range(b.n_inst)]
+    return W.from_instances(insts)
+
+
+@pytest.mark.parametrize("len_max", [12, 28, 48, 63])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_lane_kernel_profile_widths(K, ctx, oracle_mod, pol, len_max):
+    """k_mc_lane (one lane per instance) at every profile width it instantiates
+    (max_len < 16, < 32, < 52, <= 63 -> 4, 8, 13, 16 words): equal to the oracle and to
+    the one-warp-per-instance kernel (SCHED_FLAG_WARP_PER_INSTANCE)."""
+    b = W.lane_mix(4000, 40 + len_max, len_max=len_max, gap_max=6)
+    o, g = check(K, ctx, oracle_mod, b, pol, f"lane len_max={len_max}")
+    w = gpu_run(K, ctx, b, pol, flags=K.kvsched.FLAG_WARP_PER_INSTANCE)
+    assert_parity(o, w, b, "warp kernel")
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_lane_kernel_scope_edges(K, ctx, oracle_mod, pol):
+    """A batch mixing instances inside the lane kernel's scope with every kind it hands to
+    k_mc_small: n > 128, s > 7, arrival gaps > 511, o~ > o (MC-SF), invalid rows, empty
+    instances, and n = 128 / s = 7 / gaps of 511 exactly at the edges."""
+    inside = W.lane_mix(1500, 51, n_max=128, gap_max=8)
+    big_n = W.lane_mix(60, 52, n_max=400, gap_max=3)
+    big_s = W.lane_mix(300, 53, s_max=12, M_lo=20)
+    gaps = W.lane_mix(300, 54, n_max=12, gap_max=900)
+    edge = [([[0, 7, 57, 57]] * 128, 64), ([[0, 7, 1, 1], [511, 7, 1, 1], [1022, 1, 56, 56]], 64)]
+    slow = [([[0, 2, 3, 9], [0, 1, 5, 5]], 20), ([[1, 3, 4, 4], [2, 2, 2, 6]], 12)]
+    bad = [([[3, 1, 1, 1], [2, 1, 1, 1]], 10), ([[0, 1, 1, 1]] * 3, 6), ([], 7), ([[0, 5, 6, 6]], 10)]
+    b = _concat(inside, big_n, W.from_instances(edge), big_s, gaps,
+                W.from_instances(slow if pol == 0 else []), W.from_instances(bad))
+    o, g = check(K, ctx, oracle_mod, b, pol, "lane scope edges")
+    w = gpu_run(K, ctx, b, pol, flags=K.kvsched.FLAG_WARP_PER_INSTANCE)
+    assert_parity(o, w, b, "warp kernel")
+    h = gpu_run(K, ctx, b, pol, hints=(0, 0, 0))
+    assert_parity(o, h, b, "measured hints")
+
+
 @pytest.mark.parametrize("pol", [0, 1])
 def test_small_kernel_large_queues(K, ctx, oracle_mod, pol):
     """More than 1024 requests per instance with M <= 64: the fused kernel keeps the waiting

@@ -281,6 +281,26 @@ def random_small(n_inst: int, seed: int, n_max: int = 40, M_lo: int = 4, M_hi: i
     return b
 
 
+def lane_mix(n_inst: int, seed: int, len_max: int = 63, n_max: int = 128, s_max: int = 7,
+             gap_max: int = 40, M_lo: int = 8, M_hi: int = 64) -> Batch:
+    """Parity batch shaped for the one-lane-per-instance MC kernel's scope edges:
+    n~U{1..n_max}, M~U{M_lo..M_hi}, s~U{1..min(s_max, M-1)}, o~U{1..min(M-s, len_max)},
+    arrival gaps U{0..gap_max} (o~ = o).  Choosing n_max > 128, s_max > 7 or gap_max > 511
+    puts some instances outside that scope."""
+    g = _rng([17, seed, len_max, n_max, s_max, gap_max, M_lo, M_hi])
+    sizes = g.integers(1, n_max + 1, size=n_inst).astype(np.int64)
+    M = g.integers(M_lo, M_hi + 1, size=n_inst)
+    Mrep = np.repeat(M, sizes)
+    s = g.integers(1, np.minimum(s_max, Mrep - 1) + 1)
+    o = g.integers(1, np.minimum(Mrep - s, len_max) + 1)
+    gaps = g.integers(0, gap_max + 1, size=int(sizes.sum()))
+    starts = np.zeros(n_inst + 1, dtype=np.int64)
+    np.cumsum(sizes, out=starts[1:])
+    a = np.cumsum(gaps)
+    a = a - np.repeat(a[starts[:-1]], sizes) + np.repeat(g.integers(0, 50, size=n_inst), sizes)
+    return _assemble(a, s, o, sizes, M, "lane-mix", dict(seed=seed, len_max=len_max))
+
+
 def with_prediction_noise(b: Batch, eps: float, seed: int = 7) -> Batch:
     """Replace o~ by a noisy prediction o^ ~ U((1-eps)o, (1+eps)o), rounded to
     an integer >= 1 on the host (DESIGN Q26): o^ = max(1, floor(o (1 + eps (2u - 1)) + 0.5)).
