@@ -66,35 +66,81 @@ struct LaneInst {                            // one lane's instance (registers)
 };
 
 // -------------------------------------------------------------------------------------
+// Work feed of one warp.  Instances are claimed 32 at a time (one atomic); lane j holds
+// the CSR offset, size and budget of instance base + j.  The request rows of the next
+// instance to stage are loaded one refill ahead (lane l holds rows l, l+32, l+64, l+96),
+// so the global-memory latency overlaps the simulation instead of stalling the warp.
+struct LaneFeed {
+    long long base;          // first instance of the batch (warp-uniform)
+    int cnt, cur;            // batch size, next instance to stage (warp-uniform)
+    long long off;           // lane j: first row of instance base + j
+    int n, M;                // lane j: its size and budget
+    int4 r[4];               // rows of instance base + cur (prefetched)
+};
+
+__device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
+{
+    const int lane = lane_id();
+    const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
+    const int n = __shfl_sync(KV_FULL, F.n, F.cur);
+    const int m = n <= LANE_NP ? n : 0;          // out-of-scope sizes are not staged
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int k = lane + 32 * c;
+        F.r[c] = k < m ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);
+    }
+}
+
+// claim the next batch; false when the work counter is exhausted (warp-uniform)
+__device__ __forceinline__ bool feed_claim(const KParams &P, LaneFeed &F)
+{
+    const int lane = lane_id();
+    long long base = 0;
+    if (lane == 0) base = (long long)atomicAdd(P.counter, 32ull);
+    base = __shfl_sync(KV_FULL, base, 0);
+    if (base >= P.n_inst) return false;
+    F.base = base;
+    F.cnt = (int)min(32ll, P.n_inst - base);
+    F.cur = 0;
+    if (lane < F.cnt) {
+        const long long o0 = P.offset[base + lane];
+        F.off = o0 - P.row_base;
+        F.n = (int)(P.offset[base + lane + 1] - o0);
+        F.M = P.mem[base + lane];
+    } else {
+        F.off = 0;
+        F.n = 0;
+        F.M = 0;
+    }
+    feed_prefetch(P, F);
+    return true;
+}
+
 // Stage instances into the idle lanes of `idle` (warp-uniform).  Returns false once the
 // work counter is exhausted.
 template <int POL, int NW>
 __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, int *hist, LaneInst<NW> &L,
-                                            uint32_t idle)
+                                            uint32_t idle, LaneFeed &F)
 {
     const int lane = lane_id();
     uint16_t *d16 = reinterpret_cast<uint16_t *>(data);
     while (idle) {
         const int tl = __ffs(idle) - 1;
-        long long inst = 0;
-        if (lane == 0) inst = (long long)atomicAdd(P.counter, 1ull);
-        inst = __shfl_sync(KV_FULL, inst, 0);
-        if (inst >= P.n_inst) return false;
-        const long long off = P.offset[inst] - P.row_base;
-        const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
-        const int M = P.mem[inst];
+        if (F.cur >= F.cnt && !feed_claim(P, F)) return false;
+        const long long inst = F.base + F.cur;
+        const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
+        const int n = __shfl_sync(KV_FULL, F.n, F.cur);
+        const int M = __shfl_sync(KV_FULL, F.M, F.cur);
+        int4 r[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r[c] = F.r[c];
+        if (++F.cur < F.cnt) feed_prefetch(P, F);
         // in scope, and within the caller's size hints (k_mc_small reports violations)
         bool ok = n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
-        int4 r[4];
         int an[4];
         long long suma = 0;
         if (ok) {
             bool bad = false;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int k = lane + 32 * c;
-                r[c] = k < n ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);
-            }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const int k = lane + 32 * c;
@@ -326,12 +372,14 @@ __global__ void __launch_bounds__(128, 3) k_mc_lane(const KParams P)
 
     LaneInst<NW> L;
     L.active = false;
+    LaneFeed F;
+    F.cnt = F.cur = 0;
     uint32_t pk16 = 0u;
     bool more = true;
     for (;;) {
         const uint32_t idle = __ballot_sync(KV_FULL, !L.active);
         if (idle && more) {
-            more = lane_refill<POL, NW>(P, data, hist, L, idle);
+            more = lane_refill<POL, NW>(P, data, hist, L, idle, F);
             if (idle & (1u << lane)) pk16 = 0u;
         }
         if (!__any_sync(KV_FULL, L.active)) break;
