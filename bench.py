@@ -188,9 +188,9 @@ def ncu_record(kernel_name: str) -> dict:
 
 
 def issue_roofline(rec: dict, sm_mhz: float | None):
-    """The binding resource of the simulation kernels is instruction issue (one warp
-    instruction per SM sub-partition per clock: 148 SMs x 4 x f_SM).  Achieved = warp
-    instructions / duration of the committed ncu capture."""
+    """Instruction issue (one warp instruction per SM sub-partition per clock: 148 SMs x 4
+    x f_SM), reported beside the ALU-pipe roofline.  Achieved = warp instructions /
+    duration of the committed ncu capture."""
     try:
         inst = float(str(rec["warp_inst"]).replace(",", ""))
         dur = float(rec["duration_ms"]) / 1e3
@@ -304,24 +304,44 @@ def main():
     rounds_all, ok_all, inst_all = (int(x) for x in tot.tolist())
     value = rounds_all * args.steps / (ms_max / 1000.0)
 
-    # roofline of the simulation kernel: algorithmic bytes per launch / mean launch time
-    kname = ctx.last_kernel()
-    k_ms = st["sim_kernel_ms"] / max(args.steps, 1)          # simulation kernel time per step
+    # roofline of the dominant simulation kernel (most device time inside the timed region;
+    # CUDA events on the launching stream, per kernel name, from the library's accounting)
+    kst = ctx.kernel_stats()
+    kname = max(kst, key=lambda k: kst[k][0]) if kst else ctx.last_kernel()
+    k_tot_ms, k_launches = kst.get(kname, (st["sim_kernel_ms"], st["sim_kernel_launches"]))
+    k_ms = k_tot_ms / max(k_launches, 1)                    # mean duration of one launch
     alg = algorithmic_bytes(batch, fields)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak_gbs = peaks.get("hbm_gbs", 6650.0)
-    achieved = alg / (k_ms / 1000.0) / 1e9
     rec = ncu_record(kname)
-    traffic = rec.get("dram_bytes_per_launch")
-    if traffic is not None and rec.get("source", "").find("bench") < 0 and args.workload == "c5":
-        traffic = None            # captured on another launch size
-    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-            "frac": achieved / peak_gbs, "traffic": traffic, "alg_bytes_per_launch": alg,
-            "kernel_ms": k_ms, "sim_launches_per_step": st["sim_kernel_launches"] / max(args.steps, 1),
-            "peak_source": "measured" if peaks else "fallback",
-            "kernel_share_of_step": (st["sim_kernel_ms"] / args.steps) / (ms_max / args.steps) if args.steps else None,
-            "traffic_source": rec.get("source"),
-            "issue": issue_roofline(rec, None)}
+    same_launch = rec.get("source", "").find("bench") >= 0 and args.workload == "c5" and args.policy == "mcsf" \
+        and batch.n_inst == 1_000_000
+    traffic = rec.get("dram_bytes_per_launch") if same_launch else None
+    hbm = {"bound": "hbm", "achieved": alg / (k_ms / 1e3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+           "frac": alg / (k_ms / 1e3) / 1e9 / peak_gbs, "alg_bytes_per_launch": alg,
+           "peak_source": "measured" if peaks else "fallback"}
+    # The simulators are bound by the integer ALU pipe (SWAR / DPX / logic ops), not by HBM:
+    # peak = 148 SMs x 4 sub-partitions x 0.5 ALU-pipe warp instructions per clock (the
+    # guide's rt_SMSP = 2 for IADD3/LOP3/SHF/PRMT/VIMNMX) at the SM clock measured under load;
+    # achieved = the launch's ALU-pipe warp instructions (ncu capture of this same launch
+    # configuration: the work is deterministic) / the live mean launch duration.
+    f_mhz = (ck or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 4 * 0.5 * f_mhz * 1e6
+    alu_inst = rec.get("alu_inst")
+    if alu_inst is not None and same_launch:
+        alu_ach = float(str(alu_inst).replace(",", "")) / (k_ms / 1e3)
+        roof = {"bound": "alu", "kernel": kname, "achieved": alu_ach, "peak": alu_peak,
+                "unit": "ALU-pipe warp-inst/s", "frac": alu_ach / alu_peak, "traffic": traffic,
+                "peak_source": f"derived: 148 x 4 x 0.5/clk x {f_mhz:.0f} MHz (measured SM clock under load)",
+                "alu_inst_per_launch": float(str(alu_inst).replace(",", "")),
+                "alu_inst_source": rec.get("source")}
+    else:
+        roof = dict(hbm, kernel=kname, traffic=traffic)
+    roof.update(kernel_ms=k_ms, launches_per_step=k_launches / max(args.steps, 1),
+                kernel_share_of_step=(k_tot_ms / args.steps) / (ms_max / args.steps) if args.steps else None,
+                kernels={k: {"ms_per_step": v[0] / max(args.steps, 1), "launches_per_step": v[1] / max(args.steps, 1)}
+                         for k, v in kst.items()},
+                hbm=hbm, issue=issue_roofline(rec, f_mhz) if same_launch else None)
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None

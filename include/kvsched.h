@@ -250,6 +250,13 @@ int sched_get_stats(sched_ctx *ctx, int64_t *launches, double *sim_kernel_ms,
                     int64_t *sim_kernel_launches);
 int sched_reset_stats(sched_ctx *ctx);
 
+/* Per-kernel split of the same accounting: entry i (0-based, in order of first launch
+ * since the last reset) names a simulation kernel (static string) with its summed device
+ * time (ms) and launch count.  SCHED_E_ARG when i is out of range (the caller stops
+ * there).  Host pointers; any may be NULL.                                               */
+int sched_get_kernel_stats(sched_ctx *ctx, int32_t i, const char **name, double *ms,
+                           int64_t *launches);
+
 /* Name of the simulation kernel the last sched_run_instances call launched (static string). */
 const char *sched_last_kernel(const sched_ctx *ctx);
 

@@ -51,7 +51,17 @@ struct sched_ctx {
     long long launches = 0, sim_launches = 0;
     double sim_ms = 0.0;
     bool timing = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    struct Timed {
+        cudaEvent_t e0, e1;
+        const char *name;
+    };
+    struct KStat {
+        const char *name;
+        double ms;
+        long long launches;
+    };
+    std::vector<Timed> pending;
+    std::vector<KStat> kstats;
     std::vector<cudaEvent_t> free_events;
     cudaStream_t s_in = nullptr, s_out = nullptr;     // host path copy streams
     std::vector<cudaEvent_t> chunk_events;
@@ -251,7 +261,7 @@ int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const c
     CUDA_TRY(c, cudaGetLastError());
     if (c->timing) {
         CUDA_TRY(c, cudaEventRecord(e1, c->stream));
-        c->pending.emplace_back(e0, e1);
+        c->pending.push_back({e0, e1, name});
     }
     c->launches++;
     c->sim_launches++;
@@ -278,7 +288,7 @@ int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
     CUDA_TRY(c, cudaGetLastError());
     if (c->timing) {
         CUDA_TRY(c, cudaEventRecord(e1, c->stream));
-        c->pending.emplace_back(e0, e1);
+        c->pending.push_back({e0, e1, name});
     }
     c->launches++;
     c->sim_launches++;
@@ -895,22 +905,50 @@ int sched_set_timing(sched_ctx *c, int enable)
     return SCHED_OK;
 }
 
+static int drain_pending(sched_ctx *c)
+{
+    DeviceGuard g(c->device);
+    for (auto &p : c->pending) {
+        CUDA_TRY(c, cudaEventSynchronize(p.e1));
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, p.e0, p.e1));
+        c->sim_ms += ms;
+        bool found = false;
+        for (auto &k : c->kstats)
+            if (k.name == p.name || strcmp(k.name, p.name) == 0) {
+                k.ms += ms;
+                k.launches++;
+                found = true;
+                break;
+            }
+        if (!found) c->kstats.push_back({p.name, (double)ms, 1});
+        c->free_events.push_back(p.e0);
+        c->free_events.push_back(p.e1);
+    }
+    c->pending.clear();
+    return SCHED_OK;
+}
+
 int sched_get_stats(sched_ctx *c, int64_t *launches, double *sim_kernel_ms, int64_t *sim_kernel_launches)
 {
     if (!c) return SCHED_E_STATE;
-    DeviceGuard g(c->device);
-    for (auto &p : c->pending) {
-        CUDA_TRY(c, cudaEventSynchronize(p.second));
-        float ms = 0.f;
-        CUDA_TRY(c, cudaEventElapsedTime(&ms, p.first, p.second));
-        c->sim_ms += ms;
-        c->free_events.push_back(p.first);
-        c->free_events.push_back(p.second);
-    }
-    c->pending.clear();
+    int rc = drain_pending(c);
+    if (rc) return rc;
     if (launches) *launches = c->launches;
     if (sim_kernel_ms) *sim_kernel_ms = c->sim_ms;
     if (sim_kernel_launches) *sim_kernel_launches = c->sim_launches;
+    return SCHED_OK;
+}
+
+int sched_get_kernel_stats(sched_ctx *c, int32_t i, const char **name, double *ms, int64_t *launches)
+{
+    if (!c) return SCHED_E_STATE;
+    int rc = drain_pending(c);
+    if (rc) return rc;
+    if (i < 0 || (size_t)i >= c->kstats.size()) return fail(c, SCHED_E_ARG, "kernel stats index %d out of range", i);
+    if (name) *name = c->kstats[i].name;
+    if (ms) *ms = c->kstats[i].ms;
+    if (launches) *launches = c->kstats[i].launches;
     return SCHED_OK;
 }
 
@@ -922,6 +960,7 @@ int sched_reset_stats(sched_ctx *c)
     c->launches = 0;
     c->sim_launches = 0;
     c->sim_ms = 0.0;
+    c->kstats.clear();
     return rc;
 }
 
@@ -937,8 +976,8 @@ int sched_finalize(sched_ctx *c)
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
+            cudaEventDestroy(p.e0);
+            cudaEventDestroy(p.e1);
         }
         for (auto e : c->free_events) cudaEventDestroy(e);
         for (auto e : c->chunk_events) cudaEventDestroy(e);

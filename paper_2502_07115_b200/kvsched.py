@@ -29,7 +29,8 @@ EXPORTS = ("sched_abi_version", "sched_init", "sched_set_stream", "sched_run_ins
            "sched_run_instances_host", "sched_latency", "sched_lb_sorted", "sched_gen_am2_count",
            "sched_gen_am2_fill", "sched_wallclock", "sched_philox4x32_10",
            "sched_set_timing",
-           "sched_get_stats", "sched_reset_stats", "sched_last_kernel", "sched_finalize",
+           "sched_get_stats", "sched_get_kernel_stats", "sched_reset_stats", "sched_last_kernel",
+           "sched_finalize",
            "sched_last_error")
 
 P = ctypes.c_void_p
@@ -96,6 +97,8 @@ def load() -> ctypes.CDLL:
         L.sched_set_timing.argtypes = [P, ctypes.c_int]
         L.sched_get_stats.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(i64)]
+        L.sched_get_kernel_stats.argtypes = [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_char_p),
+                                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.sched_reset_stats.argtypes = [P]
         L.sched_last_kernel.argtypes = [P]
         L.sched_last_kernel.restype = ctypes.c_char_p
@@ -252,6 +255,16 @@ class Context:
         self._check(self._lib.sched_get_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
                     "sched_get_stats")
         return dict(launches=a.value, sim_kernel_ms=b.value, sim_kernel_launches=c.value)
+
+    def kernel_stats(self) -> dict:
+        """{kernel name: (device ms, launches)} since the last reset (timing enabled)."""
+        out, i = {}, 0
+        while True:
+            nm, ms, n = ctypes.c_char_p(), ctypes.c_double(), i64()
+            if self._lib.sched_get_kernel_stats(self._h, i, ctypes.byref(nm), ctypes.byref(ms), ctypes.byref(n)):
+                return out
+            out[nm.value.decode()] = (ms.value, n.value)
+            i += 1
 
     def reset_stats(self):
         self._check(self._lib.sched_reset_stats(self._h), "sched_reset_stats")

@@ -22,6 +22,10 @@ METRICS = [
     "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__inst_executed.sum",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__cycles_elapsed.avg", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "sm__inst_executed_pipe_alu.sum", "sm__inst_executed_pipe_fma.sum",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__cycles_active.sum",
 ]
 
 
@@ -30,6 +34,9 @@ POLICY = {"0": "MCSF", "1": "MCBENCH", "2": "ALPHA", "3": "ALPHA_BETA"}
 
 def abi_name(short: str) -> str:
     """ncu's demangled template name -> the name sched_last_kernel() reports."""
+    m = re.match(r"k_mc_lane<(\d), (\d+)>", short)
+    if m:
+        return f"k_mc_lane<{POLICY[m.group(1)]}>"
     m = re.match(r"k_mc_small<(\d), (\d), (\d)>", short)
     if m:
         pol, multi, qreg = m.groups()
@@ -66,6 +73,15 @@ def to_ns(v: str, unit: str) -> float:
     return x * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(unit, 1)
 
 
+def alu_inst(d: dict):
+    try:
+        pct = float(d["sm__inst_executed_pipe_alu.sum.pct_of_peak_sustained_active"].replace(",", ""))
+        cyc = float(d["sm__cycles_active.sum"].replace(",", ""))
+    except (KeyError, ValueError):
+        return None
+    return pct / 100.0 * 2.0 * cyc
+
+
 def hot_sass(rep: str, top: int):
     text = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass")
     rows = list(csv.reader(io.StringIO(text)))
@@ -74,7 +90,12 @@ def hot_sass(rep: str, top: int):
     hdr = rows[1]
     ia, isrc = hdr.index("Instructions Executed"), hdr.index("Source")
     ist = hdr.index("Warp Stall Sampling (All Samples)")
-    data = [(int(r[ia] or 0), int(r[ist] or 0), r[isrc].strip()) for r in rows[2:] if len(r) > ist]
+    data = []
+    for r in rows[2:]:
+        try:
+            data.append((int(r[ia] or 0), int(r[ist] or 0), r[isrc].strip()))
+        except (IndexError, ValueError):
+            continue
     tot = sum(d[0] for d in data)
     return sorted(data, key=lambda x: -x[1])[:top], tot
 
@@ -102,7 +123,12 @@ def main():
                           "duration_ms": dur / 1e6, "source": Path(a.rep).name,
                           "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                           "registers": d.get("launch__registers_per_thread"),
-                          "warp_inst": d.get("smsp__inst_executed.sum")}
+                          "warp_inst": d.get("smsp__inst_executed.sum"),
+                          # ALU-pipe warp instructions: ncu's percentage of the pipe's peak
+                          # (0.5 warp-inst / clk / SMSP = 2 / clk / SM) x active SM cycles
+                          "alu_inst": alu_inst(d),
+                          "fma_inst": d.get("sm__inst_executed_pipe_fma.sum"),
+                          "alu_pipe_pct": d.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")}
     hot, tot = hot_sass(a.rep, a.top)
     print(f"== hottest SASS by stall samples (total warp instructions {tot:.4g})")
     for c, s, src in hot:
