@@ -347,18 +347,24 @@ def main():
     e2e = None
     if not args.no_e2e and world >= 1:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        # rows on the wire as uint16 deltas (SCHED_REQ_U16X4_DELTA) when they fit: half the
-        # PCIe bytes; the results read back are the schedule (completion per request) and
-        # the per-instance outputs (start = completion - o is not copied)
-        pk = batch.packed_u16()
-        fmt = K.kvsched.REQ_U16X4_DELTA if pk is not None else K.kvsched.REQ_I32X4
-        rows = pk.view(np.int16) if pk is not None else batch.req
-        e2e_fields = [k for k in fields if k != "start"]
+        # Rows on the wire in the narrowest delta encoding they fit (SCHED_REQ_U8X4_DELTA: 4
+        # bytes per request on C5, else uint16 deltas, else int32); the schedule comes back as
+        # the compact latency16 (c_i - a_i, uint16 per request) plus the per-instance
+        # outputs.  start = completion - o and completion = a + latency16 are not copied.
+        pk8 = batch.packed_u8()
+        pk = pk8 if pk8 is not None else batch.packed_u16()
+        if pk8 is not None:
+            fmt, rows, fmt_name = K.kvsched.REQ_U8X4_DELTA, pk8.view(np.int8), "u8x4-delta"
+        elif pk is not None:
+            fmt, rows, fmt_name = K.kvsched.REQ_U16X4_DELTA, pk.view(np.int16), "u16x4-delta"
+        else:
+            fmt, rows, fmt_name = K.kvsched.REQ_I32X4, batch.req, "i32x4"
+        e2e_fields = [k for k in fields if k not in ("start", "completion")] + ["latency16"]
         h_off, h_req, h_mem = pin(batch.offset), pin(rows), pin(batch.mem)
         h_out = {}
         for k in e2e_fields:
-            n = batch.n_req if k in ("completion", "start") else batch.n_inst
-            dt = torch.int64 if k in K.kvsched.OUT_I64 else torch.int32
+            n = batch.n_req if k in ("completion", "start", "latency16") else batch.n_inst
+            dt = torch.int64 if k in K.kvsched.OUT_I64 else torch.int16 if k == "latency16" else torch.int32
             h_out[k] = torch.empty(max(n, 1), dtype=dt).pin_memory()
         host = {k: v.numpy() for k, v in h_out.items()}
         a_off, a_req, a_mem = h_off.numpy(), h_req.numpy(), h_mem.numpy()
@@ -376,13 +382,16 @@ def main():
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e_ms = float(e_ms.item())
-        same = np.array_equal(host["rounds"][:batch.n_inst], out["rounds"][:batch.n_inst].cpu().numpy())
+        comp_dev = out["completion"][:batch.n_req].cpu().numpy().astype(np.int64)
+        lat = host["latency16"][:batch.n_req].view(np.uint16).astype(np.int64)
+        same = bool(np.array_equal(host["rounds"][:batch.n_inst], out["rounds"][:batch.n_inst].cpu().numpy())
+                    and np.array_equal(batch.req[:, 0].astype(np.int64) + lat, comp_dev))
         h2d = rows.nbytes + (batch.n_inst + 1) * 8 + batch.n_inst * 4
         d2h = sum(v.numel() * v.element_size() for v in h_out.values())
         e2e = {"value": rounds_all * args.e2e_steps / (e_ms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": e_ms / args.e2e_steps, "matches_device_run": bool(same),
-               "req_format": "u16x4-delta" if pk is not None else "i32x4", "outputs": e2e_fields}
+               "req_format": fmt_name, "outputs": e2e_fields}
 
     ab = None
     if args.ab:

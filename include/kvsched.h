@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define KVSCHED_ABI_VERSION 1
+#define KVSCHED_ABI_VERSION 2
 
 /* return codes */
 enum {
@@ -119,7 +119,10 @@ typedef struct {
                                    count).  Not accepted by sched_latency / sched_lb_sorted.  */
 } sched_instances;
 
-enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1 };
+enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1, SCHED_REQ_U8X4_DELTA = 2 };
+/* SCHED_REQ_U8X4_DELTA: rows are uint8 {a_i - a_(i-1) (a_(-1) = 0), s_i, o_i, o~_i}, 4-byte
+ * aligned -- a quarter of the int32 bytes for batches whose gaps and sizes fit a byte (the
+ * C5 sweep); decoded on the device like SCHED_REQ_U16X4_DELTA.                           */
 /* "measure" runs a reduction kernel and synchronises the stream to read the bounds.
  * Instances that exceed a caller-given bound get status SCHED_INST_UNSUPPORTED.            */
 
@@ -148,6 +151,10 @@ typedef struct {
     int32_t *peak_mem;          /* [n_instances] max over processed rounds of the batch's KV
                                    occupancy sum (s_j + t+1 - p_j) (Eq. 3 at t+1)            */
     int32_t *status;            /* [n_instances] SCHED_INST_*                                */
+    uint16_t *latency16;        /* [n_req] compact schedule for transfers: c_i - a_i when the
+                                   request completed and c_i - a_i <= 65534, else 65535
+                                   (completion = a_i + latency16).  Computed on the device
+                                   from the completion rounds after the run (ABI version 2). */
 } sched_outputs;
 
 /* Create a context on `device` that enqueues on `cuda_stream` (a cudaStream_t; NULL = the

@@ -9,6 +9,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <utility>
 #include <vector>
 
 #include "../../include/kvsched.h"
@@ -45,7 +46,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk;
+    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk, comp;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -64,6 +65,13 @@ struct sched_ctx {
     std::vector<KStat> kstats;
     std::vector<cudaEvent_t> free_events;
     cudaStream_t s_in = nullptr, s_out = nullptr;     // host path copy streams
+    // host path: extra compute streams, each with its own per-run scratch, so that the
+    // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
+    struct RunScratch {
+        cudaStream_t stream = nullptr;
+        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp;
+    };
+    RunScratch extra[2];
     std::vector<cudaEvent_t> chunk_events;
 };
 
@@ -173,10 +181,12 @@ __global__ void __launch_bounds__(128) k_latency(long long n_inst, const long lo
     }
 }
 
-// SCHED_REQ_U16X4_DELTA -> int32 rows: one warp per instance, a_i = prefix sum of the gaps.
+// SCHED_REQ_U16X4_DELTA / SCHED_REQ_U8X4_DELTA -> int32 rows: one warp per instance, a_i =
+// prefix sum of the gaps.
 // Rows of instance k are input rows offset[k]-row_base.. and output rows likewise.
-__global__ void __launch_bounds__(128) k_decode_u16(long long n_inst, const long long *offset, long long row_base,
-                                                    const ushort4 *in, int4 *out)
+template <typename R>
+__global__ void __launch_bounds__(128) k_decode_rows(long long n_inst, const long long *offset, long long row_base,
+                                                     const R *in, int4 *out)
 {
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -185,7 +195,7 @@ __global__ void __launch_bounds__(128) k_decode_u16(long long n_inst, const long
         int carry = 0;
         for (long long b = lo; b < hi; b += 32) {
             const long long i = b + lane;
-            const ushort4 r = i < hi ? in[i] : make_ushort4(0, 0, 0, 0);
+            const R r = i < hi ? in[i] : R{0, 0, 0, 0};
             int a = r.x;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -196,6 +206,16 @@ __global__ void __launch_bounds__(128) k_decode_u16(long long n_inst, const long
             if (i < hi) out[i] = make_int4(a, r.y, r.z, r.w);
             carry = __shfl_sync(KV_FULL, a, 31);
         }
+    }
+}
+
+// completion rounds -> the compact latency16 output (c_i - a_i, 65535 = none / too large)
+__global__ void k_latency16(long long n_rows, const int4 *req, const int *completion, uint16_t *lat)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_rows; i += (long long)gridDim.x * blockDim.x) {
+        const int c = completion[i];
+        const long long d = (long long)c - req[i].x;
+        lat[i] = (c < 0 || d < 0 || d > 65534) ? (uint16_t)65535 : (uint16_t)d;
     }
 }
 
@@ -218,6 +238,20 @@ __global__ void k_philox(long long n, const uint4 *ctr, const uint2 *key, uint4 
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         out[i] = philox4x32_10(ctr[i], key[i]);
+}
+
+// exchange the context's per-run scratch and stream with a host-path compute set
+void swap_run_scratch(sched_ctx *c, sched_ctx::RunScratch &r)
+{
+    std::swap(c->stream, r.stream);
+    std::swap(c->counter, r.counter);
+    std::swap(c->bounds, r.bounds);
+    std::swap(c->rq, r.rq);
+    std::swap(c->arank, r.arank);
+    std::swap(c->pstart, r.pstart);
+    std::swap(c->relnext, r.relnext);
+    std::swap(c->retry, r.retry);
+    std::swap(c->comp, r.comp);
 }
 
 template <typename K>
@@ -301,12 +335,14 @@ int check_common(sched_ctx *c, const sched_instances *inst)
     if (!c) return SCHED_E_STATE;
     if (!inst) return fail(c, SCHED_E_ARG, "inst is NULL");
     if (inst->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
-    if (inst->req_format != SCHED_REQ_I32X4 && inst->req_format != SCHED_REQ_U16X4_DELTA)
+    if (inst->req_format != SCHED_REQ_I32X4 && inst->req_format != SCHED_REQ_U16X4_DELTA &&
+        inst->req_format != SCHED_REQ_U8X4_DELTA)
         return fail(c, SCHED_E_ARG, "unknown req_format %d", inst->req_format);
     if (inst->n_instances > 0) {
         if (!inst->req_offset || !inst->mem_limit || !inst->req)
             return fail(c, SCHED_E_ARG, "req_offset, req and mem_limit must be non-NULL");
-        if (((uintptr_t)inst->req) & (inst->req_format == SCHED_REQ_I32X4 ? 15u : 7u))
+        if (((uintptr_t)inst->req) & (inst->req_format == SCHED_REQ_I32X4 ? 15u :
+                                      inst->req_format == SCHED_REQ_U16X4_DELTA ? 7u : 3u))
             return fail(c, SCHED_E_ARG, "req is misaligned for its format");
     }
     if (inst->max_requests < 0 || inst->max_mem < 0 || inst->max_len < 0)
@@ -572,6 +608,34 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
 
 extern "C" {
 
+// latency16 = completion - a on rows [0, n_rows) (device pointers; see kvsched.h)
+static int launch_latency16(sched_ctx *c, long long n_rows, const int4 *req, const int *comp, uint16_t *lat)
+{
+    if (n_rows <= 0) return SCHED_OK;
+    long long blocks = (n_rows + 255) / 256;
+    if (blocks > 8LL * c->num_sms) blocks = 8LL * c->num_sms;
+    k_latency16<<<(int)blocks, 256, 0, c->stream>>>(n_rows, req, comp, lat);
+    CUDA_TRY(c, cudaGetLastError());
+    c->launches++;
+    return SCHED_OK;
+}
+
+// run_impl plus the compact latency16 output (needs the completion rounds: the caller's,
+// or context scratch when it did not ask for them)
+static int run_outputs(sched_ctx *c, const sched_instances *di, const sched_policy *pol, const sched_outputs *out,
+                       long long row_base, long long n_rows)
+{
+    if (!out->latency16) return run_impl(c, di, pol, out, row_base);
+    sched_outputs o = *out;
+    int rc;
+    if (!o.completion) {
+        if ((rc = grow(c, c->comp, (size_t)(n_rows > 0 ? n_rows : 1) * 4))) return rc;
+        o.completion = (int32_t *)c->comp.p;
+    }
+    if ((rc = run_impl(c, di, pol, &o, row_base))) return rc;
+    return launch_latency16(c, n_rows, reinterpret_cast<const int4 *>(di->req), o.completion, out->latency16);
+}
+
 int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_policy *pol,
                         const sched_outputs *out)
 {
@@ -581,24 +645,32 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     if (!out) return fail(c, SCHED_E_ARG, "out is NULL");
     if (inst->n_instances == 0) return SCHED_OK;
     DeviceGuard g(c->device);
-    if (inst->req_format == SCHED_REQ_U16X4_DELTA) {
-        long long n_req = 0;
+    long long n_req = 0;
+    if (inst->req_format != SCHED_REQ_I32X4 || out->latency16) {
         CUDA_TRY(c, cudaMemcpyAsync(&n_req, inst->req_offset + inst->n_instances, 8, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    if (inst->req_format != SCHED_REQ_I32X4) {
         if ((rc = grow(c, c->dec, (size_t)(n_req > 0 ? n_req : 1) * 16))) return rc;
         long long blocks = (inst->n_instances + 3) / 4;
         if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
-        k_decode_u16<<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset),
-                                                          0, reinterpret_cast<const ushort4 *>(inst->req),
-                                                          reinterpret_cast<int4 *>(c->dec.p));
+        const long long *doff = reinterpret_cast<const long long *>(inst->req_offset);
+        if (inst->req_format == SCHED_REQ_U16X4_DELTA)
+            k_decode_rows<ushort4><<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, doff, 0,
+                                                                       reinterpret_cast<const ushort4 *>(inst->req),
+                                                                       reinterpret_cast<int4 *>(c->dec.p));
+        else
+            k_decode_rows<uchar4><<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, doff, 0,
+                                                                      reinterpret_cast<const uchar4 *>(inst->req),
+                                                                      reinterpret_cast<int4 *>(c->dec.p));
         CUDA_TRY(c, cudaGetLastError());
         c->launches++;
         sched_instances di = *inst;
         di.req = (const int32_t *)c->dec.p;
         di.req_format = SCHED_REQ_I32X4;
-        return run_impl(c, &di, pol, out, 0);
+        return run_outputs(c, &di, pol, out, 0, n_req);
     }
-    return run_impl(c, inst, pol, out, 0);
+    return run_outputs(c, inst, pol, out, 0, n_req);
 }
 
 // Host buffers.  The batch is cut into chunks of whole instances; chunk k's request rows are
@@ -632,6 +704,10 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
                     const uint16_t *r = reinterpret_cast<const uint16_t *>(inst->req) + 4 * i;
                     o_ = r[2];
                     w_ = r[3];
+                } else if (inst->req_format == SCHED_REQ_U8X4_DELTA) {
+                    const uint8_t *r = reinterpret_cast<const uint8_t *>(inst->req) + 4 * i;
+                    o_ = r[2];
+                    w_ = r[3];
                 } else {
                     const int32_t *r = inst->req + 4 * i;
                     o_ = r[2];
@@ -647,22 +723,28 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         if (hi.max_mem == 0) hi.max_mem = 1;
         if (hi.max_len == 0) hi.max_len = 1;
     }
-    const bool packed = inst->req_format == SCHED_REQ_U16X4_DELTA;
-    const size_t row_in = packed ? 8 : 16;                // bytes per input row on the wire
+    const bool packed = inst->req_format != SCHED_REQ_I32X4;
+    const size_t row_in = inst->req_format == SCHED_REQ_U16X4_DELTA ? 8 : packed ? 4 : 16;   // bytes per row on the wire
     const size_t b_off = (size_t)(ni + 1) * 8, b_req = (size_t)n_req * 16, b_mem = (size_t)ni * 4;
     if ((rc = grow(c, c->h_off, b_off)) || (rc = grow(c, c->h_req, b_req)) || (rc = grow(c, c->h_mem, b_mem)))
         return rc;
     if (packed && (rc = grow(c, c->h_pk, (size_t)n_req * 8 + 8))) return rc;
-    // device outputs: completion, start [n_req] int32; 4 x int64 + 3 x int32 per instance
+    // device outputs: completion, start [n_req] int32; 4 x int64 + 3 x int32 per instance;
+    // latency16 [n_req] uint16
     const size_t o_comp = 0, o_start = o_comp + (size_t)n_req * 4, o_i64 = (o_start + (size_t)n_req * 4 + 15) & ~(size_t)15;
     const size_t o_i32 = o_i64 + (size_t)ni * 8 * 4;
-    const size_t total = o_i32 + (size_t)ni * 4 * 3;
+    const size_t o_lat = (o_i32 + (size_t)ni * 4 * 3 + 15) & ~(size_t)15;
+    const size_t total = o_lat + (size_t)n_req * 2;
     if ((rc = grow(c, c->h_out, total))) return rc;
     char *ob = (char *)c->h_out.p;
     if (!c->s_in) {
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+        for (auto &r : c->extra) CUDA_TRY(c, cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
     }
+    for (auto &r : c->extra)
+        if ((rc = grow(c, r.counter, 64)) || (rc = grow(c, r.bounds, 64))) return rc;
+    const int n_streams = 3;              // the context's stream + c->extra
     // chunks of ~4 M request rows (64 MB), at most 32 (KVSCHED_HOST_CHUNK_ROWS overrides the
     // chunk size; used by the tests to exercise the pipeline on small batches)
     long long chunk_rows = 4ll << 20;
@@ -682,18 +764,30 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     for (long long k = 0; k < n_chunks; ++k) {
         const long long i0 = ni * k / n_chunks, i1 = ni * (k + 1) / n_chunks;
         const long long r0 = hoff[i0], r1 = hoff[i1];
-        char *dst = packed ? (char *)c->h_pk.p + r0 * 8 : (char *)c->h_req.p + r0 * 16;
+        char *dst = packed ? (char *)c->h_pk.p + r0 * row_in : (char *)c->h_req.p + r0 * 16;
         const char *src = (const char *)inst->req + r0 * row_in;
         if (r1 > r0)
             CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)(r1 - r0) * row_in, cudaMemcpyHostToDevice, c->s_in));
         CUDA_TRY(c, cudaEventRecord(ev[2 * k], c->s_in));
+        // chunk k computes on stream k mod 3 (with that stream's scratch)
+        sched_ctx::RunScratch *rs = (k % n_streams) ? &c->extra[k % n_streams - 1] : nullptr;
+        if (rs) swap_run_scratch(c, *rs);
+        struct Restore {
+            sched_ctx *c;
+            sched_ctx::RunScratch *rs;
+            ~Restore() { if (rs) swap_run_scratch(c, *rs); }
+        } restore{c, rs};
         CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2 * k], 0));
         if (packed && i1 > i0) {
             long long blocks = (i1 - i0 + 3) / 4;
             if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
-            k_decode_u16<<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
-                                                              reinterpret_cast<const ushort4 *>(dst),
-                                                              reinterpret_cast<int4 *>((char *)c->h_req.p + r0 * 16));
+            int4 *rows = reinterpret_cast<int4 *>((char *)c->h_req.p + r0 * 16);
+            if (inst->req_format == SCHED_REQ_U16X4_DELTA)
+                k_decode_rows<ushort4><<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
+                                                                           reinterpret_cast<const ushort4 *>(dst), rows);
+            else
+                k_decode_rows<uchar4><<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
+                                                                          reinterpret_cast<const uchar4 *>(dst), rows);
             CUDA_TRY(c, cudaGetLastError());
             c->launches++;
         }
@@ -714,11 +808,14 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         dout.makespan = out->makespan ? (int32_t *)(ob + o_i32) + i0 : nullptr;
         dout.peak_mem = out->peak_mem ? (int32_t *)(ob + o_i32 + ni * 4) + i0 : nullptr;
         dout.status = out->status ? (int32_t *)(ob + o_i32 + ni * 8) + i0 : nullptr;
-        if (di.n_instances > 0 && (rc = run_impl(c, &di, pol, &dout, r0))) return rc;
+        dout.latency16 = out->latency16 ? (uint16_t *)(ob + o_lat) + r0 : nullptr;
+        if (dout.latency16 && !dout.completion) dout.completion = (int32_t *)(ob + o_comp) + r0;   // device scratch
+        if (di.n_instances > 0 && (rc = run_outputs(c, &di, pol, &dout, r0, r1 - r0))) return rc;
         CUDA_TRY(c, cudaEventRecord(ev[2 * k + 1], c->stream));
         CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, ev[2 * k + 1], 0));
         struct { void *h; const void *d; size_t b; } cp[] = {
             {out->completion ? out->completion + r0 : nullptr, dout.completion, (size_t)(r1 - r0) * 4},
+            {out->latency16 ? out->latency16 + r0 : nullptr, dout.latency16, (size_t)(r1 - r0) * 2},
             {out->start ? out->start + r0 : nullptr, dout.start, (size_t)(r1 - r0) * 4},
             {out->tel ? out->tel + i0 : nullptr, dout.tel, (size_t)(i1 - i0) * 8},
             {out->rounds ? out->rounds + i0 : nullptr, dout.rounds, (size_t)(i1 - i0) * 8},
@@ -732,6 +829,7 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->s_out));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (auto &r : c->extra) CUDA_TRY(c, cudaStreamSynchronize(r.stream));
     return SCHED_OK;
 }
 
@@ -972,7 +1070,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->comp, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {
@@ -981,6 +1079,11 @@ int sched_finalize(sched_ctx *c)
         }
         for (auto e : c->free_events) cudaEventDestroy(e);
         for (auto e : c->chunk_events) cudaEventDestroy(e);
+        for (auto &r : c->extra) {
+            for (DevBuf *b : {&r.counter, &r.bounds, &r.rq, &r.arank, &r.pstart, &r.relnext, &r.retry, &r.comp})
+                if (b->p) cudaFree(b->p);
+            if (r.stream) cudaStreamDestroy(r.stream);
+        }
         if (c->s_in) cudaStreamDestroy(c->s_in);
         if (c->s_out) cudaStreamDestroy(c->s_out);
     }

@@ -21,7 +21,7 @@ POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": A
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
 FLAG_WARP_PER_INSTANCE = 2
-REQ_I32X4, REQ_U16X4_DELTA = 0, 1
+REQ_I32X4, REQ_U16X4_DELTA, REQ_U8X4_DELTA = 0, 1, 2
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}
 
 # every symbol include/kvsched.h declares
@@ -61,7 +61,7 @@ class SchedClock(ctypes.Structure):
 class SchedOutputs(ctypes.Structure):
     _fields_ = [("completion", P), ("start", P), ("tel", P), ("rounds", P),
                 ("decision_rounds", P), ("evictions", P), ("makespan", P), ("peak_mem", P),
-                ("status", P)]
+                ("status", P), ("latency16", P)]
 
 
 OUT_FIELDS = ("completion", "start", "tel", "rounds", "decision_rounds", "evictions", "makespan",
@@ -179,7 +179,7 @@ class Context:
         """sched_run_instances on device tensors; `outputs` maps OUT_FIELDS names to
         preallocated device tensors (missing = not requested)."""
         si = self.instances(offset, req, mem, id0, hints, req_format)
-        so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS])
+        so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS + ("latency16",)])
         pc = policy.as_c()
         self._check(self._lib.sched_run_instances(self._h, ctypes.byref(si), ctypes.byref(pc),
                                                   ctypes.byref(so)), "sched_run_instances")
@@ -188,7 +188,7 @@ class Context:
                  outputs: dict, id0: int = 0, hints=(0, 0, 0), req_format: int = 0) -> None:
         """sched_run_instances_host on host (numpy, ideally pinned) arrays."""
         si = self.instances(offset, req, mem, id0, hints, req_format)
-        so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS])
+        so = SchedOutputs(*[_ptr(outputs.get(k)) for k in OUT_FIELDS + ("latency16",)])
         pc = policy.as_c()
         self._check(self._lib.sched_run_instances_host(self._h, ctypes.byref(si), ctypes.byref(pc),
                                                        ctypes.byref(so)), "sched_run_instances_host")
@@ -305,25 +305,30 @@ def hints_of(batch) -> tuple[int, int, int]:
 
 
 def simulate(ctx: Context, batch, policy: Policy, id0: int = 0, hints=None, fields=OUT_FIELDS,
-             packed: bool = False) -> dict:
+             packed=False, latency16: bool = False) -> dict:
     """Run a host batch on the device; returns numpy arrays trimmed to the batch size.
-    packed=True ships the rows as SCHED_REQ_U16X4_DELTA (decoded on the device)."""
+    packed=True / "u16" ships the rows as SCHED_REQ_U16X4_DELTA, "u8" as SCHED_REQ_U8X4_DELTA
+    (decoded on the device); latency16=True also requests the compact uint16 schedule."""
     import torch
     dev = torch.device("cuda", ctx.device)
     off, req, mem = to_device(batch, dev)
     fmt = REQ_I32X4
     if packed:
-        pk = batch.packed_u16()
+        pk = batch.packed_u8() if packed == "u8" else batch.packed_u16()
         if pk is None:
-            raise ValueError("batch does not fit the uint16 delta encoding")
-        req = torch.from_numpy(pk.view(np.int16) if pk.size else np.zeros((1, 4), np.int16)).to(dev)
-        fmt = REQ_U16X4_DELTA
+            raise ValueError(f"batch does not fit the {packed} delta encoding")
+        dt = np.int8 if packed == "u8" else np.int16
+        req = torch.from_numpy(pk.view(dt) if pk.size else np.zeros((1, 4), dt)).to(dev)
+        fmt = REQ_U8X4_DELTA if packed == "u8" else REQ_U16X4_DELTA
     out = alloc_outputs(batch.n_inst, batch.n_req, dev, fields)
+    if latency16:
+        out["latency16"] = torch.empty(max(batch.n_req, 1), dtype=torch.int16, device=dev)
     ctx.run(off, req, mem, policy, out, id0=id0, hints=hints if hints is not None else (0, 0, 0),
             req_format=fmt)
     torch.cuda.synchronize(dev)
     res = {}
     for k, v in out.items():
-        n = batch.n_req if k in ("completion", "start") else batch.n_inst
-        res[k] = v.cpu().numpy()[:n]
+        n = batch.n_inst if k not in ("completion", "start", "latency16") else batch.n_req
+        a = v.cpu().numpy()[:n]
+        res[k] = a.view(np.uint16) if k == "latency16" else a
     return res

@@ -27,7 +27,26 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     assert set(declared_functions()) == set(kv.EXPORTS)
-    assert lib.sched_abi_version() == 1
+    hdr = (ROOT / "include" / "kvsched.h").read_text()
+    assert lib.sched_abi_version() == int(re.search(r"#define KVSCHED_ABI_VERSION (\d+)", hdr).group(1))
+
+
+def test_binding_structs_match_the_header():
+    """The ctypes structs carry the header's fields in the header's order."""
+    import paper_2502_07115_b200.kvsched as kv
+    hdr = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "kvsched.h").read_text(), flags=re.S)
+    for cname, pyname in (("sched_outputs", kv.SchedOutputs), ("sched_instances", kv.SchedInstances),
+                          ("sched_policy", kv.SchedPolicy)):
+        body = re.search(r"typedef struct \{([^}]*)\}\s*" + cname + ";", hdr).group(1)
+        decl = []
+        for d in body.split(";"):
+            d = d.strip()
+            if not d:
+                continue
+            first, *rest = d.split(",")
+            decl.append(re.split(r"[\s*]+", first.strip())[-1])
+            decl += [x.strip().lstrip("*").strip() for x in rest]
+        assert decl == [f[0] for f in pyname._fields_], (cname, decl)
 
 
 def test_sched_init_fails_loudly_without_gpu():

@@ -96,6 +96,14 @@ class Batch:
             return None
         return np.ascontiguousarray(cols.astype(np.uint16))
 
+    def packed_u8(self):
+        """Rows as uint8 {a_i - a_(i-1), s, o, o~} (SCHED_REQ_U8X4_DELTA), or None if a value
+        does not fit a byte."""
+        pk = self.packed_u16()
+        if pk is None or (pk.size and pk.max() > 0xFF):
+            return None
+        return np.ascontiguousarray(pk.astype(np.uint8))
+
     def sha256(self) -> str:
         h = hashlib.sha256()
         for a in (self.offset, self.req, self.mem):
