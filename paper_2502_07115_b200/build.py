@@ -15,6 +15,7 @@ DEPS = sorted(CSRC.glob("*.cu*")) + [ROOT / "include" / "kvsched.h"]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v"]
+NVCC_FLAGS += os.environ.get("KVSCHED_NVCC_DEFS", "").split()   # experiments only (build(force=True))
 
 
 def nvcc() -> str:

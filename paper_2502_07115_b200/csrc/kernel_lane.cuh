@@ -37,9 +37,16 @@
 
 namespace kv {
 
-constexpr int LANE_NP = 128;                 // requests per instance on the lane path
+#ifndef KV_LANE_NP
+#define KV_LANE_NP 96
+#endif
+// Requests per instance on the lane path.  96 keeps a warp's shared memory at 14 KB (request
+// words + first-fit bytes) so that 16 warps fit an SM; on C5 ~1 % of the instances are
+// larger and run on k_mc_small.
+constexpr int LANE_NP = KV_LANE_NP;
+constexpr int LANE_NC = LANE_NP / 32;        // row chunks of 32 per instance
 constexpr int LANE_NW = 16;                  // profile words (bytes tau = 1..64)
-constexpr int LANE_WARP_BYTES = LANE_NP * 32 * 4 + 2048 + 64 * 4;   // words, F bytes, hist
+constexpr int LANE_WARP_BYTES = LANE_NP * 32 * 4 + 2048;   // request words, F bytes (+ hist in refill)
 
 __device__ __forceinline__ uint32_t rep4(int x) { return (uint32_t)x * 0x01010101u; }
 __host__ __device__ constexpr uint32_t tau_word(int i)
@@ -68,14 +75,14 @@ struct LaneInst {                            // one lane's instance (registers)
 // -------------------------------------------------------------------------------------
 // Work feed of one warp.  Instances are claimed 32 at a time (one atomic); lane j holds
 // the CSR offset, size and budget of instance base + j.  The request rows of the next
-// instance to stage are loaded one refill ahead (lane l holds rows l, l+32, l+64, l+96),
+// instance to stage are loaded one refill ahead (lane l holds rows l, l+32, l+64),
 // so the global-memory latency overlaps the simulation instead of stalling the warp.
 struct LaneFeed {
     long long base;          // first instance of the batch (warp-uniform)
     int cnt, cur;            // batch size, next instance to stage (warp-uniform)
     long long off;           // lane j: first row of instance base + j
     int n, M;                // lane j: its size and budget
-    int4 r[4];               // rows of instance base + cur (prefetched)
+    int4 r[LANE_NC];         // rows of instance base + cur (prefetched)
 };
 
 __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
@@ -85,7 +92,7 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
     const int n = __shfl_sync(KV_FULL, F.n, F.cur);
     const int m = n <= LANE_NP ? n : 0;          // out-of-scope sizes are not staged
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < LANE_NC; ++c) {
         const int k = lane + 32 * c;
         F.r[c] = k < m ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);
     }
@@ -131,21 +138,21 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
         const int n = __shfl_sync(KV_FULL, F.n, F.cur);
         const int M = __shfl_sync(KV_FULL, F.M, F.cur);
-        int4 r[4];
+        int4 r[LANE_NC];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) r[c] = F.r[c];
+        for (int c = 0; c < LANE_NC; ++c) r[c] = F.r[c];
         if (++F.cur < F.cnt) feed_prefetch(P, F);
         // in scope, and within the caller's size hints (k_mc_small reports violations)
         bool ok = n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
-        int an[4];
+        int an[LANE_NC];
         long long suma = 0;
         if (ok) {
             bool bad = false;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < LANE_NC; ++c) {
                 const int k = lane + 32 * c;
                 int nx = __shfl_down_sync(KV_FULL, r[c].x, 1);
-                const int nx0 = __shfl_sync(KV_FULL, r[c < 3 ? c + 1 : 3].x, 0);
+                const int nx0 = __shfl_sync(KV_FULL, r[c < LANE_NC - 1 ? c + 1 : LANE_NC - 1].x, 0);
                 if (lane == 31) nx = nx0;
                 an[c] = (k + 1 < n) ? nx - r[c].x : 0;           // a_(k+1) - a_k
                 if (k < n) {
@@ -168,13 +175,13 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         suma = warp_sum_i64(suma);
         const int a0 = __shfl_sync(KV_FULL, r[0].x, 0);
         // ranks: (o~, idx) order by a stable counting sort on o~ (MC-SF); idx (MC-Benchmark)
-        int rank[4];
+        int rank[LANE_NC];
         if (POL == POL_MCSF) {
             hist[lane] = 0;
             hist[lane + 32] = 0;
             __syncwarp();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < LANE_NC; ++c) {
                 const int k = lane + 32 * c;
                 const int v = k < n ? r[c].z : 64 + lane;
                 const unsigned peers = __match_any_sync(KV_FULL, v);
@@ -193,7 +200,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
             hist[2 * lane + 1] = x - h1;
             __syncwarp();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < LANE_NC; ++c) {
                 const int k = lane + 32 * c;
                 const int v = k < n ? r[c].z : 64 + lane;
                 const unsigned peers = __match_any_sync(KV_FULL, v);
@@ -204,10 +211,10 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
             }
         } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) rank[c] = lane + 32 * c;
+            for (int c = 0; c < LANE_NC; ++c) rank[c] = lane + 32 * c;
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < LANE_NC; ++c) {
             const int k = lane + 32 * c;
             if (k < n) {
                 const uint32_t key = (uint32_t)r[c].z | ((uint32_t)r[c].y << 6) | ((uint32_t)k << 9);
@@ -360,14 +367,14 @@ __device__ __forceinline__ int hmax16(uint32_t v) { return max((int)(v & 0xffffu
 
 // -------------------------------------------------------------------------------------
 template <int POL, int NW>
-__global__ void __launch_bounds__(128, 3) k_mc_lane(const KParams P)
+__global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem_raw + (size_t)warp * LANE_WARP_BYTES;
     uint32_t *data = reinterpret_cast<uint32_t *>(wbase);
     unsigned char *fcol = wbase + LANE_NP * 32 * 4 + lane * 16;   // F bytes: [4][32 lanes][16]
-    int *hist = reinterpret_cast<int *>(wbase + LANE_NP * 32 * 4 + 2048);
+    int *hist = reinterpret_cast<int *>(wbase + LANE_NP * 32 * 4);   // aliases F: refill only
     const uint32_t *col = data + lane;           // this lane's column: word k at col[32 k]
 
     LaneInst<NW> L;

@@ -151,13 +151,14 @@ def test_lane_kernel_profile_widths(K, ctx, oracle_mod, pol, len_max):
 @pytest.mark.parametrize("pol", [0, 1])
 def test_lane_kernel_scope_edges(K, ctx, oracle_mod, pol):
     """A batch mixing instances inside the lane kernel's scope with every kind it hands to
-    k_mc_small: n > 128, s > 7, arrival gaps > 511, o~ > o (MC-SF), invalid rows, empty
-    instances, and n = 128 / s = 7 / gaps of 511 exactly at the edges."""
+    k_mc_small: n > 96, s > 7, arrival gaps > 511, o~ > o (MC-SF), invalid rows, empty
+    instances, and n = 96 / s = 7 / gaps of 511 exactly at the edges."""
     inside = W.lane_mix(1500, 51, n_max=128, gap_max=8)
     big_n = W.lane_mix(60, 52, n_max=400, gap_max=3)
     big_s = W.lane_mix(300, 53, s_max=12, M_lo=20)
     gaps = W.lane_mix(300, 54, n_max=12, gap_max=900)
-    edge = [([[0, 7, 57, 57]] * 128, 64), ([[0, 7, 1, 1], [511, 7, 1, 1], [1022, 1, 56, 56]], 64)]
+    edge = [([[0, 7, 57, 57]] * 96, 64), ([[0, 7, 57, 57]] * 97, 64), ([[0, 3, 5, 5]] * 128, 64),
+            ([[0, 7, 1, 1], [511, 7, 1, 1], [1022, 1, 56, 56]], 64)]
     slow = [([[0, 2, 3, 9], [0, 1, 5, 5]], 20), ([[1, 3, 4, 4], [2, 2, 2, 6]], 12)]
     bad = [([[3, 1, 1, 1], [2, 1, 1, 1]], 10), ([[0, 1, 1, 1]] * 3, 6), ([], 7), ([[0, 5, 6, 6]], 10)]
     b = _concat(inside, big_n, W.from_instances(edge), big_s, gaps,
