@@ -91,7 +91,7 @@ enum {
 #define SCHED_FLAG_PER_ROUND 1
 /* SCHED_FLAG_WARP_PER_INSTANCE disables the one-lane-per-instance MC kernel (k_mc_lane),
  * which otherwise runs every MC-SF / MC-Benchmark instance within its scope (M <= 64,
- * n <= 128, s <= 7, o~ = o, no round cap) and hands the rest to the one-warp-per-instance
+ * n <= 96, s <= 7, o~ = o, no round cap) and hands the rest to the one-warp-per-instance
  * kernel (same results; for A/B measurement).                                           */
 #define SCHED_FLAG_WARP_PER_INSTANCE 2
 
