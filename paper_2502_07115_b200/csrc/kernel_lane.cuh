@@ -45,6 +45,7 @@ namespace kv {
 // larger and run on k_mc_small.
 constexpr int LANE_NP = KV_LANE_NP;
 constexpr int LANE_NC = LANE_NP / 32;        // row chunks of 32 per instance
+static_assert(LANE_NP <= 96, "the waiting-queue bitmap has three words");
 constexpr int LANE_NW = 16;                  // profile words (bytes tau = 1..64)
 constexpr int LANE_WARP_BYTES = LANE_NP * 32 * 4 + 2048;   // request words, F bytes (+ hist in refill)
 
@@ -65,7 +66,7 @@ __device__ __forceinline__ uint32_t sign_bytes(uint32_t m)
 template <int NW>
 struct LaneInst {                            // one lane's instance (registers)
     uint32_t P[NW];
-    uint32_t q0, q1, q2, q3;                 // waiting queue bitmap over ranks
+    uint32_t q0, q1, q2;                     // waiting queue bitmap over ranks (<= 96)
     long long inst, off, sumc, suma;
     int t, a_next, next, n, M, h, s, w, hidx;
     int maxc, peak, dr, nr;
@@ -226,7 +227,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         if (lane == tl) {
 #pragma unroll
             for (int i = 0; i < NW; ++i) L.P[i] = 0u;
-            L.q0 = L.q1 = L.q2 = L.q3 = 0u;
+            L.q0 = L.q1 = L.q2 = 0u;
             L.inst = inst;
             L.off = off;
             L.sumc = 0;
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
         // One step of this lane's instance.  No lane leaves the iteration early: the
         // profile shift at the end votes across the warp.
         int jump = 0;
+        bool admit = false;
         if (L.active) {
             // arrivals a_i <= t join R^(t)
             while (L.a_next <= L.t) {
@@ -404,7 +406,6 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
                 L.q0 |= wq == 0 ? bit : 0u;
                 L.q1 |= wq == 1 ? bit : 0u;
                 L.q2 |= wq == 2 ? bit : 0u;
-                L.q3 |= wq == 3 ? bit : 0u;
                 if (r < L.h) { L.h = r; L.hstale = true; }
                 L.a_next = (++L.next < L.n) ? L.a_next + (int)(d >> 7) : KV_INF;
             }
@@ -438,35 +439,17 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
                 }
                 // Eq. 5 for the head at this round and, if it fails, the first round it holds
                 const int D = first_fit(L.P, L.M - L.s, L.w, fcol, pk16);
-                if (D == 0) {                                      // admit: p = t, c = t + o
-                    L.dec = true;
-                    const uint32_t S4 = rep4(L.s);
-                    const uint32_t Kw = rep4(127 - L.w);
-#pragma unroll
-                    for (int i = 0; i < NW; ++i)
-                        L.P[i] = add_fma(L.P[i], add_fma(S4, tau_word(i)) & ~sign_bytes(Kw + tau_word(i)));
-                    const int c = L.t + L.w;
-                    if (P.start) P.start[L.off + L.hidx] = L.t;
-                    if (P.completion) P.completion[L.off + L.hidx] = c;
-                    L.sumc += c;
-                    L.maxc = max(L.maxc, c);
-                    const int h = L.h;
-                    const uint32_t nb = ~(1u << (h & 31));
-                    const int wq = h >> 5;
-                    L.q0 &= wq == 0 ? nb : ~0u;
-                    L.q1 &= wq == 1 ? nb : ~0u;
-                    L.q2 &= wq == 2 ? nb : ~0u;
-                    L.q3 &= wq == 3 ? nb : ~0u;
-                    L.h = L.q0 ? __ffs(L.q0) - 1
-                        : L.q1 ? 31 + __ffs(L.q1)
-                        : L.q2 ? 63 + __ffs(L.q2)
-                        : L.q3 ? 95 + __ffs(L.q3) : KV_INF;
-                    L.hstale = true;
-                } else {
-                    // rounds t .. t+D-1 are decision rounds that admit nothing.  MC-SF: an
-                    // arrival may sort before the head, so stop at the next arrival (it joins
-                    // R there); MC-Benchmark: arrivals queue behind the head.
-                    jump = (POL == POL_MCSF) ? min(D, L.a_next - L.t) : D;
+                admit = true;
+                if (D > 0) {
+                    // rounds t .. t+D-1 are decision rounds that admit nothing; the head is
+                    // admitted at t+D in this same step.  MC-SF: an arrival at or before t+D
+                    // may sort before the head, so stop at it instead (it joins R there and
+                    // the next step decides); MC-Benchmark: arrivals queue behind the head.
+                    jump = D;
+                    if (POL == POL_MCSF && L.a_next - L.t <= D) {
+                        jump = L.a_next - L.t;
+                        admit = false;
+                    }
                     L.dr += jump;
                 }
             }
@@ -475,6 +458,27 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
         if (jump > 0) {
             L.t += jump;
             L.dec = false;
+        }
+        if (admit) {                                           // p = t, c = t + o (Eq. 3)
+            L.dec = true;
+            const uint32_t S4 = rep4(L.s);
+            const uint32_t Kw = rep4(127 - L.w);
+#pragma unroll
+            for (int i = 0; i < NW; ++i)
+                L.P[i] = add_fma(L.P[i], add_fma(S4, tau_word(i)) & ~sign_bytes(Kw + tau_word(i)));
+            const int c = L.t + L.w;
+            if (P.start) P.start[L.off + L.hidx] = L.t;
+            if (P.completion) P.completion[L.off + L.hidx] = c;
+            L.sumc += c;
+            L.maxc = max(L.maxc, c);
+            const int h = L.h;
+            const uint32_t nb = ~(1u << (h & 31));
+            const int wq = h >> 5;
+            L.q0 &= wq == 0 ? nb : ~0u;
+            L.q1 &= wq == 1 ? nb : ~0u;
+            L.q2 &= wq == 2 ? nb : ~0u;
+            L.h = L.q0 ? __ffs(L.q0) - 1 : L.q1 ? 31 + __ffs(L.q1) : L.q2 ? 63 + __ffs(L.q2) : KV_INF;
+            L.hstale = true;
         }
     }
 }
