@@ -73,6 +73,36 @@ struct LaneInst {                            // one lane's instance (registers)
     bool active, dec, hstale;
 };
 
+// Size scope of the lane path (and the caller's size hints, whose violations k_mc_small
+// reports): decided from the CSR offsets and budgets alone, before any row is read.
+__device__ __forceinline__ bool lane_size_ok(const KParams &P, int n, int M)
+{
+    return n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
+}
+
+// Lists the instances outside the size scope (retry_list / retry_count of the KParams it is
+// given) so that k_mc_small can run them beside k_mc_lane; one thread per instance,
+// warp-aggregated appends.
+__global__ void k_lane_split(const KParams P)
+{
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (long long k0 = blockIdx.x * (long long)blockDim.x; k0 < P.n_inst; k0 += stride) {
+        const long long k = k0 + threadIdx.x;
+        bool out = false;
+        if (k < P.n_inst) {
+            const long long n = P.offset[k + 1] - P.offset[k];
+            out = !lane_size_ok(P, n > 0x7fffffffll ? 0x7fffffff : (int)n, P.mem[k]);
+        }
+        const unsigned m = __ballot_sync(KV_FULL, out);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(P.retry_count, (unsigned long long)__popc(m));
+        base = __shfl_sync(KV_FULL, base, __ffs(m) - 1);
+        if (out) P.retry_list[base + __popc(m & ((1u << lane) - 1u))] = k;
+    }
+}
+
 // -------------------------------------------------------------------------------------
 // Work feed of one warp.  Instances are claimed 32 at a time (one atomic); lane j holds
 // the CSR offset, size and budget of instance base + j.  The request rows of the next
@@ -144,10 +174,12 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         for (int c = 0; c < LANE_NC; ++c) r[c] = F.r[c];
         if (++F.cur < F.cnt) feed_prefetch(P, F);
         // in scope, and within the caller's size hints (k_mc_small reports violations)
-        bool ok = n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
+        // instances outside the size scope were listed by k_lane_split before this launch
+        if (!lane_size_ok(P, n, M)) continue;
+        bool ok = true;
         int an[LANE_NC];
         long long suma = 0;
-        if (ok) {
+        {
             bool bad = false;
 #pragma unroll
             for (int c = 0; c < LANE_NC; ++c) {

@@ -65,6 +65,9 @@ struct sched_ctx {
     std::vector<KStat> kstats;
     std::vector<cudaEvent_t> free_events;
     cudaStream_t s_in = nullptr, s_out = nullptr;     // host path copy streams
+    cudaStream_t s_side = nullptr;                    // k_mc_small beside k_mc_lane (device path)
+    cudaEvent_t ev_split = nullptr, ev_side = nullptr;
+    bool side_ok = false;                             // run_impl may use s_side (device path only)
     // host path: extra compute streams, each with its own per-run scratch, so that the
     // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
     struct RunScratch {
@@ -488,11 +491,36 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         const bool qreg = P.NP <= 1024;          // waiting queue fits one word per lane
         if (!per_round && !(pol->flags & SCHED_FLAG_WARP_PER_INSTANCE) && pol->round_cap <= 0 &&
             (size_t)LANE_WARP_BYTES * 4 <= c->max_smem_optin) {
-            // one lane per instance; instances outside its scope are listed for k_mc_small
-            if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
-            P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
-            P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
-            CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
+            // One lane per instance.  Instances outside its size scope (n > 96, M > 64, hint
+            // violations) are listed first by k_lane_split and run by k_mc_small on a side
+            // stream: that launch waits for free SM slots, so it fills the lane kernel's tail
+            // instead of following it.  Instances the lane kernel rejects on their rows
+            // (s > 7, o~ != o, gaps, invalid) are listed by it and run by k_mc_small after.
+            const size_t ni = (size_t)inst->n_instances;
+            if ((rc = grow(c, c->retry, 128 + 2 * ni * 8))) return rc;
+            unsigned long long *cnt = reinterpret_cast<unsigned long long *>(c->retry.p);
+            long long *list_b = reinterpret_cast<long long *>((char *)c->retry.p + 128);
+            long long *list_a = list_b + ni;
+            CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 64, c->stream));
+            {
+                KParams S = P;
+                S.retry_list = list_a;
+                S.retry_count = cnt + 1;
+                long long blocks = (inst->n_instances + 255) / 256;
+                if (blocks > 8LL * c->num_sms) blocks = 8LL * c->num_sms;
+                k_lane_split<<<(int)(blocks > 0 ? blocks : 1), 256, 0, c->stream>>>(S);
+                CUDA_TRY(c, cudaGetLastError());
+                c->launches++;
+            }
+            const bool side = c->side_ok;
+            if (side) {
+                if (!c->s_side) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking));
+                if (!c->ev_split) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_split, cudaEventDisableTiming));
+                if (!c->ev_side) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+                CUDA_TRY(c, cudaEventRecord(c->ev_split, c->stream));
+            }
+            P.retry_count = cnt;
+            P.retry_list = list_b;
             // profile words: bytes tau = 1 .. 4 NW with byte 4 NW - 1 never reached by a window
             const int nw = max_len < 16 ? 4 : max_len < 32 ? 8 : max_len < 52 ? 13 : 16;
             const bool sf = pol->policy == SCHED_MCSF;
@@ -501,11 +529,42 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             rc = nw == 4 ? KV_LANE(4) : nw == 8 ? KV_LANE(8) : nw == 13 ? KV_LANE(13) : KV_LANE(16);
 #undef KV_LANE
             if (rc) return rc;
-            P.work_list = P.retry_list;
-            P.work_count = P.retry_count;
             P.retry_list = nullptr;
             P.retry_count = nullptr;
-            CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+            auto small = [&](const KParams &Q) -> int {
+                if (per_round) return SCHED_E_STATE;           // not reached: per-round skips the lane path
+                if (pol->policy == SCHED_MCSF)
+                    return qreg ? launch_sim(c, k_mc_small<POL_MCSF, true, true>, Q, smem, "k_mc_small<MCSF>")
+                                : launch_sim(c, k_mc_small<POL_MCSF, true, false>, Q, smem, "k_mc_small<MCSF,smemq>");
+                return qreg ? launch_sim(c, k_mc_small<POL_MCBENCH, true, true>, Q, smem, "k_mc_small<MCBENCH>")
+                            : launch_sim(c, k_mc_small<POL_MCBENCH, true, false>, Q, smem, "k_mc_small<MCBENCH,smemq>");
+            };
+            // list A (size scope): beside the lane kernel on the side stream, or after it
+            KParams A = P;
+            A.work_list = list_a;
+            A.work_count = cnt + 1;
+            A.counter = cnt + 2;
+            if (side) {
+                std::swap(c->stream, c->s_side);
+                rc = cudaStreamWaitEvent(c->stream, c->ev_split, 0) == cudaSuccess ? small(A)
+                         : fail(c, SCHED_E_CUDA, "cudaStreamWaitEvent failed");
+                if (!rc && cudaEventRecord(c->ev_side, c->stream) != cudaSuccess)
+                    rc = fail(c, SCHED_E_CUDA, "cudaEventRecord failed");
+                std::swap(c->stream, c->s_side);
+            } else {
+                rc = small(A);
+            }
+            if (rc) return rc;
+            // list B (rows out of scope; usually empty): a small grid after the lane kernel
+            KParams B = P;
+            B.work_list = list_b;
+            B.work_count = cnt;
+            B.counter = cnt + 3;
+            B.n_inst = std::min<long long>(P.n_inst, 8LL * c->num_sms);   // grid size only
+            rc = small(B);
+            if (rc) return rc;
+            if (side) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_side, 0));
+            return SCHED_OK;
         }
 #define KV_SMALL(POLV, MULTIV, QREGV, NAME) launch_sim(c, k_mc_small<POLV, MULTIV, QREGV>, P, smem, NAME)
         if (pol->policy == SCHED_MCSF) {
@@ -668,9 +727,15 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
         sched_instances di = *inst;
         di.req = (const int32_t *)c->dec.p;
         di.req_format = SCHED_REQ_I32X4;
-        return run_outputs(c, &di, pol, out, 0, n_req);
+        c->side_ok = true;
+        rc = run_outputs(c, &di, pol, out, 0, n_req);
+        c->side_ok = false;
+        return rc;
     }
-    return run_outputs(c, inst, pol, out, 0, n_req);
+    c->side_ok = true;
+    rc = run_outputs(c, inst, pol, out, 0, n_req);
+    c->side_ok = false;
+    return rc;
 }
 
 // Host buffers.  The batch is cut into chunks of whole instances; chunk k's request rows are
@@ -1084,6 +1149,9 @@ int sched_finalize(sched_ctx *c)
                 if (b->p) cudaFree(b->p);
             if (r.stream) cudaStreamDestroy(r.stream);
         }
+        if (c->s_side) cudaStreamDestroy(c->s_side);
+        if (c->ev_split) cudaEventDestroy(c->ev_split);
+        if (c->ev_side) cudaEventDestroy(c->ev_side);
         if (c->s_in) cudaStreamDestroy(c->s_in);
         if (c->s_out) cudaStreamDestroy(c->s_out);
     }
