@@ -4,34 +4,34 @@
 // positions in parallel, but every control step (queue pop, head decode, loop tests) is
 // executed by all 32 lanes for that one instance.  For small budgets (M <= 64) the whole
 // projected profile fits in 64 bytes, so here each lane runs its own instance and holds
-// its profile in 16 registers, four rounds per register (SWAR bytes):
+// its profile in NW registers, four rounds per register (SWAR bytes):
 //
-//   byte tau-1 of P[0..15] = Prof(t + tau), tau = 1..64   (Eq. 5 LHS for the in-flight S)
+//   byte tau-1 of P[0..NW-1] = Prof(t + tau)          (Eq. 5 LHS for the in-flight S)
 //
-// Eq. 5 for the head (s, w):  Prof(t+tau) + s + tau <= M  for tau in [1, w].
-// With G = Prof + tau <= M + 63 <= 127 one 32-bit add per word evaluates four rounds:
-//   y = P[i] + tau_i + (127 - (M - s))      -> bit 7 of a byte set  <=>  G > M - s
-//   m =        tau_i + (127 - w)            -> bit 7 of a byte set  <=>  tau > w
-// and the head fits iff no byte has bit 7 of (y & ~m) set (no byte ever carries: every
-// sum stays below 256).  Admission (Eq. 3) adds the ramp s + tau on tau <= w; the
-// clock advances by a one-byte funnel shift.  Rounds are stepped one at a time (no
-// look-ahead); the 32 lanes of a warp step 32 instances in lock step.
+// One loop iteration is one event of the lane's instance.  For the queue head (s, w)
+// first_fit() returns the first round offset D at which Eq. 5 holds while the profile only
+// advances -- D = 0: it fits now -- by an exact prefix-maximum fixpoint (see there).  The
+// lane then jumps D rounds (all decision rounds that admit nothing) and admits the
+// head at the landing round in the same iteration (ramp s + tau on tau <= w, Eq. 3 P:105,
+// four bytes per add); MC-SF stops the jump early at an arrival that might sort before the
+// head.  Rounds with an empty queue are skipped to the next arrival.  The 32 lanes of a
+// warp run 32 instances in lock step; a lane whose instance ends is refilled by the warp.
 //
-// Waiting queue R^(t): a 128-bit rank bitmap in four registers (rank = position in
+// Waiting queue R^(t): a 96-bit rank bitmap in three registers (rank = position in
 // (o~, idx) order for MC-SF; idx for MC-Benchmark).  Per-request words live
-// in shared memory, column `lane` of a [128][32] u32 array (bank = lane: conflict-free):
+// in shared memory, column `lane` of a [96][32] u32 array (bank = lane: conflict-free):
 //   low half  at position = rank : key {w:6 | s:3 | idx:7}
 //   high half at position = idx  : {rank:7 | a_(idx+1) - a_idx : 9}
-// Instances are claimed one lane at a time from the persistent work counter; the warp
-// stages a claimed instance cooperatively (coalesced 16-byte row loads, stable counting
-// sort on o~ for the MC-SF ranks) into the idle lane's column.
+// Instances are claimed 32 per atomic; the warp stages a claimed instance cooperatively
+// (coalesced 16-byte row loads prefetched one refill ahead, stable counting sort on o~ for
+// the MC-SF ranks) into the idle lane's column.
 //
-// Scope (checked per instance while staging): 1 <= n <= 128, M <= 64, 1 <= s <= 7,
-// o~ = o for MC-SF, s + o <= M, arrivals sorted with gaps <= 511, and no user round cap
-// (default cap: MC rounds never exceed max_a + sum o, so the cap is never reached).
-// Every other instance -- including invalid ones, whose status the general kernel
-// assigns -- is appended to a list that k_mc_small then runs.  Outputs are identical to
-// k_mc_small's (and the oracle's) field by field.
+// Scope (checked per instance): 1 <= n <= 96, M <= 64, 1 <= s <= 7, o~ = o for MC-SF,
+// s + o <= M, arrivals sorted with gaps <= 511, the caller's size hints, and no user round
+// cap (MC rounds never exceed max_a + sum o, so the default cap is never reached).  Size
+// violations are listed before the launch (k_lane_split), row violations -- including
+// invalid instances, whose status the general kernel assigns -- by the kernel; k_mc_small
+// runs both lists.  Outputs are identical to k_mc_small's (and the oracle's) field by field.
 #pragma once
 #include "params.cuh"
 
