@@ -347,13 +347,16 @@ def main():
     e2e = None
     if not args.no_e2e and world >= 1:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        # Rows on the wire in the narrowest delta encoding they fit (SCHED_REQ_U8X4_DELTA: 4
-        # bytes per request on C5, else uint16 deltas, else int32); the schedule comes back as
+        # Rows on the wire in the narrowest encoding they fit (SCHED_REQ_P16: 2 bytes per
+        # request on C5, else uint8 / uint16 deltas, else int32); the schedule comes back as
         # the compact latency16 (c_i - a_i, uint16 per request) plus the per-instance
         # outputs.  start = completion - o and completion = a + latency16 are not copied.
-        pk8 = batch.packed_u8()
+        pk16 = batch.packed_p16()
+        pk8 = batch.packed_u8() if pk16 is None else None
         pk = pk8 if pk8 is not None else batch.packed_u16()
-        if pk8 is not None:
+        if pk16 is not None:
+            fmt, rows, fmt_name = K.kvsched.REQ_P16, pk16.view(np.int16), "p16"
+        elif pk8 is not None:
             fmt, rows, fmt_name = K.kvsched.REQ_U8X4_DELTA, pk8.view(np.int8), "u8x4-delta"
         elif pk is not None:
             fmt, rows, fmt_name = K.kvsched.REQ_U16X4_DELTA, pk.view(np.int16), "u16x4-delta"

@@ -119,7 +119,11 @@ typedef struct {
                                    count).  Not accepted by sched_latency / sched_lb_sorted.  */
 } sched_instances;
 
-enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1, SCHED_REQ_U8X4_DELTA = 2 };
+enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1, SCHED_REQ_U8X4_DELTA = 2, SCHED_REQ_P16 = 3 };
+/* SCHED_REQ_P16: one uint16 per request, bits 0-5 = o_i - 1, bits 6-8 = s_i - 1, bits 9-15 =
+ * a_i - a_(i-1) (a_(-1) = 0), and o~_i = o_i (the paper's experiments) -- 2 bytes per
+ * request for batches with o <= 64, s <= 8 and arrival gaps <= 127 (the C5 sweep);
+ * 2-byte aligned; decoded on the device.                                                 */
 /* SCHED_REQ_U8X4_DELTA: rows are uint8 {a_i - a_(i-1) (a_(-1) = 0), s_i, o_i, o~_i}, 4-byte
  * aligned -- a quarter of the int32 bytes for batches whose gaps and sizes fit a byte (the
  * C5 sweep); decoded on the device like SCHED_REQ_U16X4_DELTA.                           */

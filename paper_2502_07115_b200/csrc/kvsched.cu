@@ -187,6 +187,15 @@ __global__ void __launch_bounds__(128) k_latency(long long n_inst, const long lo
 // SCHED_REQ_U16X4_DELTA / SCHED_REQ_U8X4_DELTA -> int32 rows: one warp per instance, a_i =
 // prefix sum of the gaps.
 // Rows of instance k are input rows offset[k]-row_base.. and output rows likewise.
+// the wire rows as {gap, s, o, o~}
+__device__ __forceinline__ int4 unpack_row(ushort4 r) { return make_int4(r.x, r.y, r.z, r.w); }
+__device__ __forceinline__ int4 unpack_row(uchar4 r) { return make_int4(r.x, r.y, r.z, r.w); }
+__device__ __forceinline__ int4 unpack_row(uint16_t v)     // SCHED_REQ_P16: {o-1:6 | s-1:3 | gap:7}
+{
+    const int o = (v & 63) + 1;
+    return make_int4(v >> 9, ((v >> 6) & 7) + 1, o, o);
+}
+
 template <typename R>
 __global__ void __launch_bounds__(128) k_decode_rows(long long n_inst, const long long *offset, long long row_base,
                                                      const R *in, int4 *out)
@@ -198,7 +207,7 @@ __global__ void __launch_bounds__(128) k_decode_rows(long long n_inst, const lon
         int carry = 0;
         for (long long b = lo; b < hi; b += 32) {
             const long long i = b + lane;
-            const R r = i < hi ? in[i] : R{0, 0, 0, 0};
+            const int4 r = i < hi ? unpack_row(in[i]) : make_int4(0, 0, 0, 0);
             int a = r.x;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -210,6 +219,22 @@ __global__ void __launch_bounds__(128) k_decode_rows(long long n_inst, const lon
             carry = __shfl_sync(KV_FULL, a, 31);
         }
     }
+}
+
+// decode any packed format into int32 rows on the context's stream
+static void launch_decode(sched_ctx *c, int fmt, long long n_inst, const long long *doff, long long row_base,
+                          const void *in, int4 *out)
+{
+    long long blocks = (n_inst + 3) / 4;
+    if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
+    if (blocks < 1) blocks = 1;
+    if (fmt == SCHED_REQ_U16X4_DELTA)
+        k_decode_rows<ushort4><<<(int)blocks, 128, 0, c->stream>>>(n_inst, doff, row_base, (const ushort4 *)in, out);
+    else if (fmt == SCHED_REQ_U8X4_DELTA)
+        k_decode_rows<uchar4><<<(int)blocks, 128, 0, c->stream>>>(n_inst, doff, row_base, (const uchar4 *)in, out);
+    else
+        k_decode_rows<uint16_t><<<(int)blocks, 128, 0, c->stream>>>(n_inst, doff, row_base, (const uint16_t *)in, out);
+    c->launches++;
 }
 
 // completion rounds -> the compact latency16 output (c_i - a_i, 65535 = none / too large)
@@ -339,13 +364,14 @@ int check_common(sched_ctx *c, const sched_instances *inst)
     if (!inst) return fail(c, SCHED_E_ARG, "inst is NULL");
     if (inst->n_instances < 0) return fail(c, SCHED_E_ARG, "n_instances < 0");
     if (inst->req_format != SCHED_REQ_I32X4 && inst->req_format != SCHED_REQ_U16X4_DELTA &&
-        inst->req_format != SCHED_REQ_U8X4_DELTA)
+        inst->req_format != SCHED_REQ_U8X4_DELTA && inst->req_format != SCHED_REQ_P16)
         return fail(c, SCHED_E_ARG, "unknown req_format %d", inst->req_format);
     if (inst->n_instances > 0) {
         if (!inst->req_offset || !inst->mem_limit || !inst->req)
             return fail(c, SCHED_E_ARG, "req_offset, req and mem_limit must be non-NULL");
         if (((uintptr_t)inst->req) & (inst->req_format == SCHED_REQ_I32X4 ? 15u :
-                                      inst->req_format == SCHED_REQ_U16X4_DELTA ? 7u : 3u))
+                                      inst->req_format == SCHED_REQ_U16X4_DELTA ? 7u :
+                                      inst->req_format == SCHED_REQ_U8X4_DELTA ? 3u : 1u))
             return fail(c, SCHED_E_ARG, "req is misaligned for its format");
     }
     if (inst->max_requests < 0 || inst->max_mem < 0 || inst->max_len < 0)
@@ -711,17 +737,8 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     }
     if (inst->req_format != SCHED_REQ_I32X4) {
         if ((rc = grow(c, c->dec, (size_t)(n_req > 0 ? n_req : 1) * 16))) return rc;
-        long long blocks = (inst->n_instances + 3) / 4;
-        if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
-        const long long *doff = reinterpret_cast<const long long *>(inst->req_offset);
-        if (inst->req_format == SCHED_REQ_U16X4_DELTA)
-            k_decode_rows<ushort4><<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, doff, 0,
-                                                                       reinterpret_cast<const ushort4 *>(inst->req),
-                                                                       reinterpret_cast<int4 *>(c->dec.p));
-        else
-            k_decode_rows<uchar4><<<(int)blocks, 128, 0, c->stream>>>(inst->n_instances, doff, 0,
-                                                                      reinterpret_cast<const uchar4 *>(inst->req),
-                                                                      reinterpret_cast<int4 *>(c->dec.p));
+        launch_decode(c, inst->req_format, inst->n_instances, reinterpret_cast<const long long *>(inst->req_offset), 0,
+                      inst->req, reinterpret_cast<int4 *>(c->dec.p));
         CUDA_TRY(c, cudaGetLastError());
         c->launches++;
         sched_instances di = *inst;
@@ -773,6 +790,8 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
                     const uint8_t *r = reinterpret_cast<const uint8_t *>(inst->req) + 4 * i;
                     o_ = r[2];
                     w_ = r[3];
+                } else if (inst->req_format == SCHED_REQ_P16) {
+                    o_ = w_ = (reinterpret_cast<const uint16_t *>(inst->req)[i] & 63) + 1;
                 } else {
                     const int32_t *r = inst->req + 4 * i;
                     o_ = r[2];
@@ -789,7 +808,8 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         if (hi.max_len == 0) hi.max_len = 1;
     }
     const bool packed = inst->req_format != SCHED_REQ_I32X4;
-    const size_t row_in = inst->req_format == SCHED_REQ_U16X4_DELTA ? 8 : packed ? 4 : 16;   // bytes per row on the wire
+    const size_t row_in = inst->req_format == SCHED_REQ_U16X4_DELTA ? 8 : inst->req_format == SCHED_REQ_U8X4_DELTA ? 4
+                          : packed ? 2 : 16;                                  // bytes per row on the wire
     const size_t b_off = (size_t)(ni + 1) * 8, b_req = (size_t)n_req * 16, b_mem = (size_t)ni * 4;
     if ((rc = grow(c, c->h_off, b_off)) || (rc = grow(c, c->h_req, b_req)) || (rc = grow(c, c->h_mem, b_mem)))
         return rc;
@@ -844,17 +864,9 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         } restore{c, rs};
         CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2 * k], 0));
         if (packed && i1 > i0) {
-            long long blocks = (i1 - i0 + 3) / 4;
-            if (blocks > 32LL * c->num_sms) blocks = 32LL * c->num_sms;
-            int4 *rows = reinterpret_cast<int4 *>((char *)c->h_req.p + r0 * 16);
-            if (inst->req_format == SCHED_REQ_U16X4_DELTA)
-                k_decode_rows<ushort4><<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
-                                                                           reinterpret_cast<const ushort4 *>(dst), rows);
-            else
-                k_decode_rows<uchar4><<<(int)blocks, 128, 0, c->stream>>>(i1 - i0, doff + i0, r0,
-                                                                          reinterpret_cast<const uchar4 *>(dst), rows);
+            launch_decode(c, inst->req_format, i1 - i0, doff + i0, r0, dst,
+                          reinterpret_cast<int4 *>((char *)c->h_req.p + r0 * 16));
             CUDA_TRY(c, cudaGetLastError());
-            c->launches++;
         }
         sched_instances di = hi;
         di.req_format = SCHED_REQ_I32X4;

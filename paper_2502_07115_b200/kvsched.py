@@ -21,7 +21,7 @@ POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": A
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
 FLAG_WARP_PER_INSTANCE = 2
-REQ_I32X4, REQ_U16X4_DELTA, REQ_U8X4_DELTA = 0, 1, 2
+REQ_I32X4, REQ_U16X4_DELTA, REQ_U8X4_DELTA, REQ_P16 = 0, 1, 2, 3
 ERRORS = {-1: "SCHED_E_ARG", -2: "SCHED_E_CUDA", -3: "SCHED_E_NOMEM", -4: "SCHED_E_STATE"}
 
 # every symbol include/kvsched.h declares
@@ -307,19 +307,19 @@ def hints_of(batch) -> tuple[int, int, int]:
 def simulate(ctx: Context, batch, policy: Policy, id0: int = 0, hints=None, fields=OUT_FIELDS,
              packed=False, latency16: bool = False) -> dict:
     """Run a host batch on the device; returns numpy arrays trimmed to the batch size.
-    packed=True / "u16" ships the rows as SCHED_REQ_U16X4_DELTA, "u8" as SCHED_REQ_U8X4_DELTA
-    (decoded on the device); latency16=True also requests the compact uint16 schedule."""
+    packed=True / "u16" ships the rows as SCHED_REQ_U16X4_DELTA, "u8" as SCHED_REQ_U8X4_DELTA,
+    "p16" as SCHED_REQ_P16 (decoded on the device); latency16=True also requests the compact uint16 schedule."""
     import torch
     dev = torch.device("cuda", ctx.device)
     off, req, mem = to_device(batch, dev)
     fmt = REQ_I32X4
     if packed:
-        pk = batch.packed_u8() if packed == "u8" else batch.packed_u16()
+        pk = {"u8": batch.packed_u8, "p16": batch.packed_p16}.get(packed, batch.packed_u16)()
         if pk is None:
-            raise ValueError(f"batch does not fit the {packed} delta encoding")
+            raise ValueError(f"batch does not fit the {packed} encoding")
         dt = np.int8 if packed == "u8" else np.int16
         req = torch.from_numpy(pk.view(dt) if pk.size else np.zeros((1, 4), dt)).to(dev)
-        fmt = REQ_U8X4_DELTA if packed == "u8" else REQ_U16X4_DELTA
+        fmt = {"u8": REQ_U8X4_DELTA, "p16": REQ_P16}.get(packed, REQ_U16X4_DELTA)
     out = alloc_outputs(batch.n_inst, batch.n_req, dev, fields)
     if latency16:
         out["latency16"] = torch.empty(max(batch.n_req, 1), dtype=torch.int16, device=dev)

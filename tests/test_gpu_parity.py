@@ -573,38 +573,46 @@ def _expected_latency16(o, b):
     return np.where((c < 0) | (d < 0) | (d > 65534), 65535, d).astype(np.uint16)
 
 
+@pytest.mark.parametrize("fmt", ["u8", "p16"])
 @pytest.mark.parametrize("pol", [0, 1, 2, 4])
-def test_packed_u8_rows_and_latency16(K, ctx, oracle_mod, pol, monkeypatch):
-    """SCHED_REQ_U8X4_DELTA rows (a quarter of the int32 bytes) and the compact latency16
-    output (c_i - a_i as uint16; 65535 for unfinished requests): device-pointer call and
-    chunked host path, with and without the int32 completion output beside it."""
+def test_packed_rows_and_latency16(K, ctx, oracle_mod, pol, fmt, monkeypatch):
+    """SCHED_REQ_U8X4_DELTA rows (a quarter of the int32 bytes), SCHED_REQ_P16 rows (an
+    eighth; o~ = o) and the compact latency16 output (c_i - a_i as uint16; 65535 for
+    unfinished requests): device-pointer call and chunked host path, with and without the
+    int32 completion output beside it."""
     import paper_2502_07115_b200.kvsched as kv
-    b = W.random_small(1500, 120 + pol, n_max=50, M_lo=6, M_hi=120, a_max=200)
-    b = _concat(b, W.from_instances([([[0, 5, 6, 6]], 10), ([[0, 1, 1, 1], [0, 9, 2, 2]], 10)]))
+    if fmt == "p16" and pol == 4:
+        return                                    # P16 carries o~ = o only
+    if fmt == "u8":
+        b = W.random_small(1500, 120 + pol, n_max=50, M_lo=6, M_hi=120, a_max=200)
+    else:
+        b = W.lane_mix(1500, 130 + pol, len_max=63, s_max=8, gap_max=20)
+    b = _concat(b, W.from_instances([([[0, 5, 6, 6]], 10), ([[0, 1, 1, 1], [0, 8, 2, 2]], 10)]))
     if pol == 4:
         b = W.with_prediction_noise(b, 0.3, seed=3)
-    assert b.packed_u8() is not None
+    pk = b.packed_u8() if fmt == "u8" else b.packed_p16()
+    assert pk is not None
     kw = dict(alpha=(1, 10)) if pol >= 2 else {}
     o = oracle_run(oracle_mod, b, pol, **kw)
     want = _expected_latency16(o, b)
     assert (want == 65535).any()
     p = K.Policy(KIND[pol], kw.get("alpha", (0, 1)))
-    g = K.simulate(ctx, b, p, hints=K.hints_of(b), packed="u8", latency16=True)
-    assert_parity(o, g, b, "u8 rows, device")
+    g = K.simulate(ctx, b, p, hints=K.hints_of(b), packed=fmt, latency16=True)
+    assert_parity(o, g, b, f"{fmt} rows, device")
     assert np.array_equal(g["latency16"], want)
-    g2 = K.simulate(ctx, b, p, hints=K.hints_of(b), packed="u8", latency16=True, fields=("tel", "status"))
+    g2 = K.simulate(ctx, b, p, hints=K.hints_of(b), packed=fmt, latency16=True, fields=("tel", "status"))
     assert np.array_equal(g2["latency16"], want)
     monkeypatch.setenv("KVSCHED_HOST_CHUNK_ROWS", "1000")
-    pk = b.packed_u8()
+    rf = kv.REQ_U8X4_DELTA if fmt == "u8" else kv.REQ_P16
     for with_comp in (True, False):
         outs = _host_outputs(b)
         if not with_comp:
             del outs["completion"], outs["start"]
         outs["latency16"] = np.empty(b.n_req, np.uint16)
-        ctx.run_host(b.offset, pk, b.mem, p, outs, hints=K.hints_of(b), req_format=kv.REQ_U8X4_DELTA)
+        ctx.run_host(b.offset, pk, b.mem, p, outs, hints=K.hints_of(b), req_format=rf)
         assert np.array_equal(outs["latency16"], want), with_comp
         if with_comp:
-            assert_parity(o, outs, b, "u8 rows, host chunks")
+            assert_parity(o, outs, b, f"{fmt} rows, host chunks")
         else:
             assert np.array_equal(outs["tel"], np.asarray(o["tel"]))
 

@@ -104,6 +104,19 @@ class Batch:
             return None
         return np.ascontiguousarray(pk.astype(np.uint8))
 
+    def packed_p16(self):
+        """Rows as uint16 {o-1:6 | s-1:3 | a_i - a_(i-1):7} with o~ = o (SCHED_REQ_P16), or
+        None if the batch does not fit that encoding."""
+        if self.n_req == 0:
+            return np.zeros(0, np.uint16)
+        pk = self.packed_u16()
+        if pk is None:
+            return None
+        gap, s, o, op = (pk[:, j].astype(np.int64) for j in range(4))
+        if (op != o).any() or o.min() < 1 or o.max() > 64 or s.min() < 1 or s.max() > 8 or gap.max() > 127:
+            return None
+        return np.ascontiguousarray(((o - 1) | ((s - 1) << 6) | (gap << 9)).astype(np.uint16))
+
     def sha256(self) -> str:
         h = hashlib.sha256()
         for a in (self.offset, self.req, self.mem):
