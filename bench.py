@@ -240,10 +240,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # KVSCHED_BENCH_BACKEND=gloo + KVSCHED_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo --
+    # only to exercise the multi-rank code path on a one-GPU box (never a measurement)
+    if os.environ.get("KVSCHED_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("KVSCHED_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     batch, cfg = make_workload(args.workload, args.instances, rank)
     if args.policy == "mcsf_protected":
@@ -259,13 +267,14 @@ def main():
     id0 = rank * batch.n_inst
     if world > 1:
         from paper_2502_07115_b200 import dist as D
+        res_dtype = D.result_dtype(batch)
 
     def step():
         ctx.run(off, req, mem, pol, out, id0=id0, hints=hints)
         if world > 1:
             # the north star's only collective: gather per-instance (TEL, rounds, status) of
             # every shard and reduce the totals (NCCL over NVLink / NVSwitch)
-            D.gather_results(D.pack_results(out, batch.n_inst, batch.n_inst, dev))
+            D.gather_results(D.pack_results(out, batch.n_inst, batch.n_inst, dev, res_dtype))
             D.reduce_totals(out, batch.n_inst)
 
     for _ in range(max(args.warmup, 0)):

@@ -39,7 +39,7 @@ def _worker(rank, world, port, q):
         o = oracle.simulate_batch(sub.offset, sub.req, sub.mem, oracle.ALPHA_BETA, alpha=(1, 10),
                                   beta_thresh=W.beta_threshold(0.3), seed=11, gid0=lo, nthreads=1)
         out = {k: torch.from_numpy(np.asarray(o[k], dtype=np.int64)) for k in ("tel", "rounds", "status")}
-        local = D.pack_results(out, hi - lo, max(sizes), "cpu")
+        local = D.pack_results(out, hi - lo, max(sizes), "cpu", D.result_dtype(sub))
         g = D.gather_results(local)
         tot = D.reduce_totals(out, hi - lo)
         if rank == 0:
@@ -81,3 +81,11 @@ def test_gloo_world2_gather_equals_whole_batch():
     assert np.array_equal(rows[2], whole["status"])
     ok = whole["status"] == 0
     assert tot.tolist() == [int(whole["tel"][ok].sum()), int(whole["rounds"][ok].sum()), int(ok.sum()), b.n_inst]
+
+
+def test_result_dtype_bound():
+    from paper_2502_07115_b200 import dist as D
+    assert D.result_dtype(W.am2(200, 3)) == torch.int32
+    big = W.from_instances([([[0, 1, 30000, 30000]] * 80000, 2**20)])
+    assert D.result_dtype(big) == torch.int64
+    assert D.result_dtype(W.from_instances([([], 7)])) == torch.int32
