@@ -269,7 +269,7 @@ int sched_get_kernel_stats(sched_ctx *ctx, int32_t i, const char **name, double 
                            int64_t *launches);
 
 /* Name of the simulation kernel the last sched_run_instances call launched (static string). */
-const char *sched_last_kernel(const sched_ctx *ctx);
+const char *sched_last_kernel(const sched_ctx *ctx);   /* the main one when a call launches several */
 
 /* Release the context's scratch and the context.                                         */
 int sched_finalize(sched_ctx *ctx);

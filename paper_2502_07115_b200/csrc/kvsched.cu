@@ -590,6 +590,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             rc = small(B);
             if (rc) return rc;
             if (side) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_side, 0));
+            c->last_kernel = sf ? "k_mc_lane<MCSF>" : "k_mc_lane<MCBENCH>";   // the main kernel of the call
             return SCHED_OK;
         }
 #define KV_SMALL(POLV, MULTIV, QREGV, NAME) launch_sim(c, k_mc_small<POLV, MULTIV, QREGV>, P, smem, NAME)
