@@ -72,6 +72,12 @@ class Batch:
         lo, hi = int(self.offset[k]), int(self.offset[k + 1])
         return self.req[lo:hi], int(self.mem[k])
 
+    def slice(self, lo: int, hi: int) -> "Batch":
+        """Instances lo..hi-1 as a batch (contiguous: array views, no per-instance work)."""
+        r0, r1 = int(self.offset[lo]), int(self.offset[hi])
+        return Batch(self.offset[lo:hi + 1] - r0, self.req[r0:r1], self.mem[lo:hi],
+                     self.name + "[slice]", dict(self.meta))
+
     def subset(self, ks) -> "Batch":
         ks = np.asarray(ks, dtype=np.int64)
         rows = [self.req[self.offset[k]:self.offset[k + 1]] for k in ks]
