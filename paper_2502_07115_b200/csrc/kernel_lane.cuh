@@ -509,7 +509,10 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
             L.q0 &= wq == 0 ? nb : ~0u;
             L.q1 &= wq == 1 ? nb : ~0u;
             L.q2 &= wq == 2 ? nb : ~0u;
-            L.h = L.q0 ? __ffs(L.q0) - 1 : L.q1 ? 31 + __ffs(L.q1) : L.q2 ? 63 + __ffs(L.q2) : KV_INF;
+            // next head: lowest set rank (independent selects, no branches)
+            int nh = L.q2 ? 63 + __ffs(L.q2) : KV_INF;
+            nh = L.q1 ? 31 + __ffs(L.q1) : nh;
+            L.h = L.q0 ? __ffs(L.q0) - 1 : nh;
             L.hstale = true;
         }
     }

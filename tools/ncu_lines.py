@@ -27,10 +27,15 @@ for r in csv.reader(text.splitlines()):
     except ValueError:
         c = 0
     st = int(r[4]) if r[4].isdigit() else 0
+    try:
+        th = int(r[8])                      # thread instructions executed
+    except (ValueError, IndexError):
+        th = 0
     if c > 0:
-        out.append((c, st, cur, r[0], r[1].strip()[:90]))
+        out.append((c, st, th, cur, r[0], r[1].strip()[:80]))
 tot = sum(x[0] for x in out) or 1
 tst = sum(x[1] for x in out) or 1
-print(f"total warp instructions {tot}, stall samples {tst}")
-for c, st, f, l, src in sorted(out, key=lambda x: -x[0])[:top]:
-    print(f"{c / tot * 100:5.1f}% stall {st / tst * 100:5.1f}%  {f}:{l:>4}  {src}")
+tth = sum(x[2] for x in out)
+print(f"total warp instructions {tot}, stall samples {tst}, active lanes per instruction {tth / tot:.1f}")
+for c, st, th, f, l, src in sorted(out, key=lambda x: -x[0])[:top]:
+    print(f"{c / tot * 100:5.1f}% stall {st / tst * 100:5.1f}% lanes {th / c:4.1f}  {f}:{l:>4}  {src}")
