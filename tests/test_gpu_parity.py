@@ -652,3 +652,23 @@ def test_full_size_c5_sampled(K, ctx, oracle_mod):
         assert np.array_equal(o["completion"], g["completion"][lo:hi])
         assert o["tel"] == g["tel"][k] and o["rounds"] == g["rounds"][k]
         assert o["peak"] == g["peak_mem"][k] and o["decision_rounds"] == g["decision_rounds"][k]
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_full_size_c5_every_instance(K, ctx, oracle_mod, pol):
+    """The bench configuration at full size (10^6 AM2 instances, 5 * 10^7 requests), every
+    output of every instance against the oracle (the oracle runs on all host cores)."""
+    b = W.am2(1_000_000, 5)
+    g = gpu_run(K, ctx, b, pol)
+    o = oracle_run(oracle_mod, b, pol)
+    assert_parity(o, g, b, f"C5 full, policy {pol}")
+
+
+@pytest.mark.parametrize("name,pol,alpha,beta", W.C4_POLICIES, ids=[p[0] for p in W.C4_POLICIES])
+def test_c4_large_every_instance(K, ctx, oracle_mod, name, pol, alpha, beta):
+    """C4 (trace-shaped, 1000 requests per instance) at 10^4 instances per Table-1 policy,
+    every output of every instance against the oracle."""
+    b = W.c4(10_000, 4)
+    polid = {"mcsf": 0, "mcbench": 1, "alpha": 2, "alpha_beta": 3}[pol]
+    kw = dict(alpha=alpha or (0, 1), beta_thresh=W.beta_threshold(beta or 0.0), seed=2025)
+    check(K, ctx, oracle_mod, b, polid, f"C4 10^4 {name}", **kw)
