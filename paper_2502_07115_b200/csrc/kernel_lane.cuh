@@ -305,6 +305,20 @@ __device__ __forceinline__ uint32_t max_bytes16(const uint32_t (&P)[NW], uint32_
     return acc;
 }
 
+// ... of the bytes tau = 1..d only (a superset of whole words; the rest stay in P and are
+// folded later), in tiers so that the common short gaps fold one or two words
+template <int NW>
+__device__ __forceinline__ uint32_t max_bytes16_prefix(const uint32_t (&P)[NW], uint32_t acc, int d)
+{
+    if (d <= 4)
+        return __vimax3_s16x2_relu(acc, __byte_perm(P[0], 0u, 0x4240), __byte_perm(P[0], 0u, 0x4341));
+    if (d <= 8) {
+        acc = __vimax3_s16x2_relu(acc, __byte_perm(P[0], 0u, 0x4240), __byte_perm(P[0], 0u, 0x4341));
+        return __vimax3_s16x2_relu(acc, __byte_perm(P[1], 0u, 0x4240), __byte_perm(P[1], 0u, 0x4341));
+    }
+    return max_bytes16(P, acc);
+}
+
 // P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau).  Byte 4 NW - 1 is
 // always zero (every window ends before it), so d >= 4 NW - 1 clears the profile.  The
 // word stages are predicated moves (FMA pipe), skipped by the whole warp when no lane
@@ -443,10 +457,10 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
             }
 
             if (L.h == KV_INF) {
-                // R empty: every projected byte is final (no admission can add to it); fold
-                // them into the peak before they are shifted out
-                pk16 = max_bytes16(L.P, pk16);
+                // R empty: every projected byte is final (no admission can add to it); the
+                // ones about to leave the profile are folded into the peak first
                 if (L.next == L.n) {                         // R and arrivals exhausted: drain S
+                    pk16 = max_bytes16(L.P, pk16);
                     if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
                     else L.nr += max(0, L.maxc - L.t);
                     L.peak = max(L.peak, hmax16(pk16));
@@ -457,6 +471,7 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
                 } else {
                     // rounds t .. a_next-1: S only (non-idle while t < maxc), no decision
                     const int tn = L.a_next;
+                    pk16 = max_bytes16_prefix(L.P, pk16, min(tn, L.maxc) - L.t);
                     if (L.dec) { ++L.dr; L.nr += max(0, min(tn, L.maxc) - L.t - 1); }
                     else L.nr += max(0, min(tn, L.maxc) - L.t);
                     jump = tn - L.t;
