@@ -31,6 +31,9 @@ constexpr int kSmallMaxRequests = 16384;      // 14-bit idx in the packed word
 #ifndef KV_RING_SHORT
 #define KV_RING_SHORT 2048                    // ring window of the first k_ring launch
 #endif
+#ifndef KV_PROT_SHORT
+#define KV_PROT_SHORT 1024                    // ... and of the first k_prot launch
+#endif
 
 struct DevBuf {
     void *p = nullptr;
@@ -612,7 +615,9 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     // rerun by a second launch whose ring covers every request plus the 32-round look-ahead.
     P.NP = next_pow2(max_req < 32 ? 32 : max_req);
     const int L_full = next_pow2(max_len + 33);
-    int ring_short = KV_RING_SHORT;                  // KVSCHED_RING_WINDOW: experiments only
+    // the protected kernel keeps three per-warp rings: a 1024-slot window doubles its
+    // occupancy (measured 1.48x faster on C4 with eps = 0.2 than 2048, 512 is slower)
+    int ring_short = pol->policy == SCHED_MCSF_PROTECTED ? KV_PROT_SHORT : KV_RING_SHORT;   // KVSCHED_RING_WINDOW: experiments only
     if (const char *e = getenv("KVSCHED_RING_WINDOW")) {
         const int v = atoi(e);
         if (v >= 64 && (v & (v - 1)) == 0) ring_short = v;
