@@ -35,9 +35,11 @@
  *   - Unless a function says "host", every pointer is a CUDA device pointer on the context's
  *     device, caller-owned; the library never retains or frees caller memory.
  *   - Work is enqueued asynchronously on the context's stream; nothing synchronises the host
- *     unless stated (sched_run_instances synchronises when a size hint is 0, for packed rows,
- *     and -- on the shared-memory ring path -- when n_instances x max_requests rows of scratch
- *     would exceed 256 MB, to read the true row count).
+ *     unless stated (sched_run_instances synchronises when a size hint is 0, for packed rows
+ *     or a latency16 output, and -- on the shared-memory ring path -- when n_instances x
+ *     max_requests rows of scratch would exceed 256 MB, to read the true row count).  The
+ *     MC policies may also use a library-owned side stream, joined back into the context's
+ *     stream before the call's work on it ends.
  *   - Argument errors are detected synchronously, nothing is enqueued, a negative SCHED_E_*
  *     is returned and sched_last_error() describes it.  Per-instance data problems never
  *     fail the call: they set that instance's status (SCHED_INST_*).
@@ -75,9 +77,10 @@ enum {
                                   or o~ < o; other policies: s+o > M (DESIGN Q8)          */
     SCHED_INST_LIVELOCK = 2,   /* round cap passed, or alpha head-of-line blocked for ever   */
     SCHED_INST_UNSUPPORTED = 3 /* instance exceeds the caller's size hints / kernel limits
-                                  (also: more than 32 requests longer than the 2048-round
-                                  ring window in flight at once when the full-length ring of
-                                  the rerun does not fit shared memory)                    */
+                                  (also: more than 32 requests longer than the ring window
+                                  -- 2048 rounds, 1024 for SCHED_MCSF_PROTECTED -- in flight
+                                  at once when the full-length ring of the rerun does not
+                                  fit shared memory)                                       */
 };
 
 /* Limits of this build (sched_run_instances returns SCHED_E_ARG beyond them). */
