@@ -77,7 +77,7 @@ struct sched_ctx {
         cudaStream_t stream = nullptr;
         DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp;
     };
-    RunScratch extra[2];
+    RunScratch extra[5];
     std::vector<cudaEvent_t> chunk_events;
 };
 
@@ -835,7 +835,10 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     }
     for (auto &r : c->extra)
         if ((rc = grow(c, r.counter, 64)) || (rc = grow(c, r.bounds, 64))) return rc;
-    const int n_streams = 3;              // the context's stream + c->extra
+    // compute streams: the context's stream + c->extra (measured on C5: 4 beats 2 and 3 by
+    // 4-15 %, 6 is no better); KVSCHED_HOST_STREAMS overrides (experiments)
+    int n_streams = 4;
+    if (const char *e = getenv("KVSCHED_HOST_STREAMS")) n_streams = atoi(e) >= 1 && atoi(e) <= 6 ? atoi(e) : 4;
     // chunks of ~4 M request rows (64 MB), at most 32 (KVSCHED_HOST_CHUNK_ROWS overrides the
     // chunk size; used by the tests to exercise the pipeline on small batches)
     long long chunk_rows = 4ll << 20;
