@@ -71,13 +71,14 @@ struct sched_ctx {
     cudaStream_t s_side = nullptr;                    // k_mc_small beside k_mc_lane (device path)
     cudaEvent_t ev_split = nullptr, ev_side = nullptr;
     bool side_ok = false;                             // run_impl may use s_side (device path only)
+    int lane_grid_div = 1;                            // host path: lane grid = full occupancy / this
     // host path: extra compute streams, each with its own per-run scratch, so that the
     // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
     struct RunScratch {
         cudaStream_t stream = nullptr;
         DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp;
     };
-    RunScratch extra[5];
+    RunScratch extra[7];
     std::vector<cudaEvent_t> chunk_events;
 };
 
@@ -343,6 +344,10 @@ int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
     int grid = 1;
     int rc = occupancy_grid(c, kernel, block, smem, (P.n_inst + 31) / 32, &grid);
     if (rc) return rc;
+    // the host path runs several chunks' lane kernels at once: each gets a share of the SMs,
+    // so it has several instances per lane and a short tail
+    if (c->lane_grid_div > 1) grid = grid / c->lane_grid_div > c->num_sms ? grid / c->lane_grid_div
+                                     : (grid < c->num_sms ? grid : c->num_sms);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         e0 = take_event(c);
@@ -838,7 +843,17 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
     // compute streams: the context's stream + c->extra (measured on C5: 4 beats 2 and 3 by
     // 4-15 %, 6 is no better); KVSCHED_HOST_STREAMS overrides (experiments)
     int n_streams = 4;
-    if (const char *e = getenv("KVSCHED_HOST_STREAMS")) n_streams = atoi(e) >= 1 && atoi(e) <= 6 ? atoi(e) : 4;
+    if (const char *e = getenv("KVSCHED_HOST_STREAMS")) n_streams = atoi(e) >= 1 && atoi(e) <= 8 ? atoi(e) : 4;
+    // each chunk's lane kernel gets 1/4 of the SMs (several instances per lane, short tail;
+    // the four compute streams keep the GPU full): e2e 5.7 -> 5.0 ms on C5 (2, 6, 8 measured
+    // no better); KVSCHED_HOST_GRID_DIV overrides (experiments)
+    int grid_div = 4;
+    if (const char *e = getenv("KVSCHED_HOST_GRID_DIV")) grid_div = atoi(e) >= 1 ? atoi(e) : 4;
+    struct GridDiv {
+        sched_ctx *c;
+        ~GridDiv() { c->lane_grid_div = 1; }
+    } gd{c};
+    c->lane_grid_div = grid_div;
     // chunks of ~4 M request rows (64 MB), at most 32 (KVSCHED_HOST_CHUNK_ROWS overrides the
     // chunk size; used by the tests to exercise the pipeline on small batches)
     long long chunk_rows = 4ll << 20;
