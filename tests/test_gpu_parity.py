@@ -617,6 +617,21 @@ def test_packed_rows_and_latency16(K, ctx, oracle_mod, pol, fmt, monkeypatch):
             assert np.array_equal(outs["tel"], np.asarray(o["tel"]))
 
 
+@pytest.mark.parametrize("pol", [0, 1])
+def test_host_path_lane_chunks(K, ctx, oracle_mod, pol, monkeypatch):
+    """The host path on a lane-kernel batch cut into many chunks: four compute streams, each
+    chunk's lane kernel on a quarter grid, size-scope fallbacks (n > 96) in every chunk."""
+    import paper_2502_07115_b200.kvsched as kv
+    monkeypatch.setenv("KVSCHED_HOST_CHUNK_ROWS", "4000")
+    b = _concat(W.am2(3000, 140 + pol), W.lane_mix(200, 141 + pol, n_max=130, gap_max=3))
+    o = oracle_run(oracle_mod, b, pol)
+    outs = _host_outputs(b)
+    outs["latency16"] = np.empty(b.n_req, np.uint16)
+    ctx.run_host(b.offset, b.req, b.mem, K.Policy(KIND[pol]), outs, hints=K.hints_of(b))
+    assert_parity(o, outs, b, "host lane chunks")
+    assert np.array_equal(outs["latency16"], _expected_latency16(o, b))
+
+
 def test_host_path(K, ctx, oracle_mod):
     """sched_run_instances_host (host buffers, copies inside the call) gives the same bytes."""
     import paper_2502_07115_b200.kvsched as kv
