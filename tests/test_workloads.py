@@ -75,3 +75,24 @@ def test_counter_generator_spec():
     # shards of the global id range concatenate to the whole
     x, y = W.am2_counter(2000, spec, id0=123), W.am2_counter(3000, spec, id0=2123)
     assert np.array_equal(np.concatenate([x.req, y.req]), b.req)
+
+
+def test_packed_formats_roundtrip_and_slice():
+    """The wire encodings decode back to the int32 rows (host-side check of the formats the
+    C ABI accepts), and contiguous slices equal index subsets."""
+    b = W.am2(3000, 7)
+    for pk, width in ((b.packed_u16(), 16), (b.packed_u8(), 8)):
+        assert pk is not None
+        a = np.zeros(b.n_req, np.int64)
+        for k in range(b.n_inst):
+            lo, hi = int(b.offset[k]), int(b.offset[k + 1])
+            a[lo:hi] = np.cumsum(pk[lo:hi, 0].astype(np.int64))
+        assert np.array_equal(a, b.req[:, 0]) and np.array_equal(pk[:, 1:].astype(np.int32), b.req[:, 1:])
+    p16 = b.packed_p16().astype(np.int64)
+    assert np.array_equal((p16 & 63) + 1, b.req[:, 2]) and np.array_equal(((p16 >> 6) & 7) + 1, b.req[:, 1])
+    gaps = p16 >> 9
+    assert np.array_equal(gaps, b.packed_u16()[:, 0].astype(np.int64))
+    assert W.with_prediction_noise(b, 0.3).packed_p16() is None        # o~ != o does not fit P16
+    s = b.slice(100, 250)
+    t = b.subset(range(100, 250))
+    assert np.array_equal(s.offset, t.offset) and np.array_equal(s.req, t.req) and np.array_equal(s.mem, t.mem)
