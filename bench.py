@@ -272,16 +272,45 @@ def main():
         from paper_2502_07115_b200 import dist as D
         res_dtype = D.result_dtype(batch)
 
+    # N > 1: the north star's only collective -- every rank gathers the per-instance
+    # (TEL, rounds, status) of all shards and all ranks reduce the totals (NCCL over NVLink /
+    # NVSwitch).  Each step packs its results on the compute stream into one of two
+    # buffers and runs the collectives on a side stream, so step k's exchange overlaps step
+    # k+1's kernels; a buffer is repacked only after its previous exchange has finished, and
+    # the timed region ends after the last exchange.
+    if world > 1:
+        coll = torch.cuda.Stream(dev)
+        packed = [None, None]
+        done_ev = [None, None]
+        nstep = [0]
+
     def step():
         ctx.run(off, req, mem, pol, out, id0=id0, hints=hints)
         if world > 1:
-            # the north star's only collective: gather per-instance (TEL, rounds, status) of
-            # every shard and reduce the totals (NCCL over NVLink / NVSwitch)
-            D.gather_results(D.pack_results(out, batch.n_inst, batch.n_inst, dev, res_dtype))
-            D.reduce_totals(out, batch.n_inst)
+            j = nstep[0] % 2
+            nstep[0] += 1
+            if done_ev[j] is not None:
+                stream.wait_event(done_ev[j])
+            packed[j] = D.pack_results(out, batch.n_inst, batch.n_inst, dev, res_dtype)
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            packed[j].record_stream(coll)               # allocator: in use on the side stream
+            with torch.cuda.stream(coll):
+                coll.wait_event(ready)
+                D.gather_results(packed[j])
+                D.reduce_totals({k: packed[j][i] for i, k in enumerate(D.RESULT_ROWS)}, batch.n_inst)
+                done_ev[j] = torch.cuda.Event()
+                done_ev[j].record(coll)
+
+    def join_collectives():
+        if world > 1:
+            for ev in done_ev:
+                if ev is not None:
+                    stream.wait_event(ev)
 
     for _ in range(max(args.warmup, 0)):
         step()
+    join_collectives()
     torch.cuda.synchronize(dev)
     rounds_rank = int(out["rounds"][:batch.n_inst].clamp(min=0).sum().item())
     ok_rank = int((out["status"][:batch.n_inst] == 0).sum().item())
@@ -299,6 +328,7 @@ def main():
     e0.record(stream)
     for _ in range(args.steps):
         step()
+    join_collectives()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
