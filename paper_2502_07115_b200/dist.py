@@ -81,7 +81,7 @@ def reduce_totals(out: dict, n_local: int, group=None) -> torch.Tensor:
         torch.where(ok, out["tel"][:n_local], torch.zeros_like(out["tel"][:n_local])).sum(),
         torch.where(ok, out["rounds"][:n_local], torch.zeros_like(out["rounds"][:n_local])).sum(),
         ok.sum().to(torch.int64),
-        torch.tensor(n_local, dtype=torch.int64, device=ok.device),
+        torch.full((), n_local, dtype=torch.int64, device=ok.device),   # a fill, no host copy
     ])
     if dist.is_initialized():
         dist.all_reduce(tot, group=group)
