@@ -1,0 +1,208 @@
+// kernel_flat.cuh -- MC-SF / MC-Benchmark, one LANE per instance, for instances whose
+// requests all arrive in the same round (Arrival Model 1; configuration C2) and
+// that are too large for k_mc_lane's shared-memory columns.
+//
+// With every request present from the first round, the waiting queue R^(t) is always a
+// suffix of the policy's order -- (o~, idx) for MC-SF, idx for MC-Benchmark
+// -- because Algorithm 1 admits the longest feasible prefix and nothing
+// ever joins.  So the queue is one integer (the next rank h), and the per-request keys are
+// read from global memory one at a time, in rank order, one admission ahead; no per-request
+// shared memory is needed and any n (up to the build's limit) fits.  Everything else is
+// k_mc_lane's: the byte-SWAR register profile, the exact first-fit fixpoint (first_fit),
+// one jump + the admission at its landing round per loop iteration, the peak fold.
+//
+// Staging (warp-cooperative, per claimed instance): the rows are read once, coalesced;
+// the instance is checked (all a equal, s >= 1, 1 <= o < 4 NW, o~ = o for MC-SF, s + o <=
+// M, M <= 64, the caller's hints) and, for MC-SF, ranked by a stable counting sort on o~
+// (<= 63, __match_any_sync per 32 rows); the packed keys {w:6 | s:6 | idx:15} are written in
+// rank order to global scratch.  Instances that fail the checks go to k_mc_small.
+#pragma once
+#include "kernel_lane.cuh"
+
+namespace kv {
+
+template <int NW>
+struct FlatInst {
+    uint32_t P[NW];
+    uint32_t key;                // key of rank h (s, w, idx)
+    long long inst, off, sumc, suma;
+    int t, n, M, h, maxc, peak, dr, nr;
+    bool active, dec;
+};
+
+// Stage the next instance of the work list into lane tl (warp-uniform).  false when the
+// list is exhausted.
+template <int POL, int NW>
+__device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, int *hist, FlatInst<NW> &L, int tl)
+{
+    const int lane = lane_id();
+    const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+    for (;;) {
+        long long w = 0;
+        if (lane == 0) w = (long long)atomicAdd(P.counter, 1ull);
+        w = __shfl_sync(KV_FULL, w, 0);
+        if (w >= n_work) return false;
+        const long long inst = P.work_list ? P.work_list[w] : w;
+        const long long off = P.offset[inst] - P.row_base;
+        const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
+        const int M = P.mem[inst];
+        bool ok = n >= 1 && n <= 32767 && M <= 64 && n <= P.max_requests && M <= P.max_mem;
+        int a0 = 0;
+        if (ok) {
+            a0 = P.req[off].x;
+            bool bad = false;
+            for (int k = lane; k < n; k += 32) {
+                const int4 r = P.req[off + k];
+                bad |= r.x != a0 || r.x < 0 || r.y < 1 || r.z < 1 || r.y + r.z > M || r.z >= 4 * NW;
+                if (POL == POL_MCSF) bad |= r.w != r.z;
+            }
+            ok = !__any_sync(KV_FULL, bad);
+        }
+        if (!ok) {                                              // k_mc_small runs it
+            if (lane == 0) {
+                const unsigned long long slot = atomicAdd(P.retry_count, 1ull);
+                P.retry_list[slot] = inst;
+            }
+            continue;
+        }
+        // keys in policy order: stable counting sort on o~ (MC-SF), idx order (MC-Benchmark)
+        if (POL == POL_MCSF) {
+            hist[lane] = 0;
+            hist[lane + 32] = 0;
+            __syncwarp();
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const int v = k < n ? P.req[off + k].z : 64 + lane;
+                const unsigned peers = __match_any_sync(KV_FULL, v);
+                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                __syncwarp();
+            }
+            const int h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+            int x = h0 + h1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(KV_FULL, x, d);
+                if (lane >= d) x += y;
+            }
+            __syncwarp();
+            hist[2 * lane] = x - h0 - h1;
+            hist[2 * lane + 1] = x - h1;
+            __syncwarp();
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const int4 r = k < n ? P.req[off + k] : make_int4(0, 0, 0, 0);
+                const int v = k < n ? r.z : 64 + lane;
+                const unsigned peers = __match_any_sync(KV_FULL, v);
+                if (k < n) {
+                    const int rk = hist[v] + __popc(peers & ((1u << lane) - 1u));
+                    keys[off + rk] = (uint32_t)r.z | ((uint32_t)r.y << 6) | ((uint32_t)k << 12);
+                }
+                __syncwarp();
+                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                __syncwarp();
+            }
+        } else {
+            for (int k = lane; k < n; k += 32) {
+                const int4 r = P.req[off + k];
+                keys[off + k] = (uint32_t)r.z | ((uint32_t)r.y << 6) | ((uint32_t)k << 12);
+            }
+        }
+        __threadfence_block();
+        __syncwarp();
+        const uint32_t first = keys[off];
+        if (lane == tl) {
+#pragma unroll
+            for (int i = 0; i < NW; ++i) L.P[i] = 0u;
+            L.key = first;
+            L.inst = inst;
+            L.off = off;
+            L.sumc = 0;
+            L.suma = (long long)a0 * n;
+            L.t = a0;
+            L.n = n;
+            L.M = M;
+            L.h = 0;
+            L.maxc = -1;
+            L.peak = 0;
+            L.dr = L.nr = 0;
+            L.active = true;
+            L.dec = false;
+        }
+        return true;
+    }
+}
+
+template <int POL, int NW>
+__global__ void __launch_bounds__(128, 4) k_mc_flat(const KParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *wbase = smem_raw + (size_t)warp * 2048;
+    unsigned char *fcol = wbase + lane * 16;                 // F bytes: [4][32 lanes][16]
+    int *hist = reinterpret_cast<int *>(wbase);              // aliases F: staging only
+    uint32_t *keys = P.flat_keys;                            // [rows] keys in policy order
+
+    FlatInst<NW> L;
+    L.active = false;
+    uint32_t pk16 = 0u;
+    bool more = true;
+    for (;;) {
+        uint32_t idle = __ballot_sync(KV_FULL, !L.active);
+        while (idle && more) {
+            const int tl = __ffs(idle) - 1;
+            more = flat_refill<POL, NW>(P, keys, hist, L, tl);
+            if (lane == tl) pk16 = 0u;
+            idle &= idle - 1;
+        }
+        if (!__any_sync(KV_FULL, L.active)) break;
+
+        int jump = 0;
+        bool admit = false;
+        if (L.active) {
+            if (L.h == L.n) {                                // every request admitted: drain S
+                pk16 = max_bytes16(L.P, pk16);
+                if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
+                else L.nr += max(0, L.maxc - L.t);
+                L.peak = max(L.peak, hmax16(pk16));
+                if (P.tel) P.tel[L.inst] = L.sumc - L.suma;
+                if (P.rounds) P.rounds[L.inst] = (long long)(L.dr + L.nr);
+                if (P.drounds) P.drounds[L.inst] = (long long)L.dr;
+                if (P.evictions) P.evictions[L.inst] = 0;
+                if (P.makespan) P.makespan[L.inst] = L.maxc;
+                if (P.peak) P.peak[L.inst] = L.peak;
+                if (P.status) P.status[L.inst] = ST_OK;
+                L.active = false;
+            } else {
+                // Eq. 5 for the head at this round and, if it fails, the first round it holds;
+                // the rounds before it are decision rounds that admit nothing (no arrivals)
+                const int w = (int)(L.key & 63u), s = (int)((L.key >> 6) & 63u);
+                const int D = first_fit(L.P, L.M - s, w, fcol, pk16);
+                jump = D;
+                L.dr += D;
+                admit = true;
+            }
+        }
+        shift_bytes(L.P, jump);                              // all 32 lanes (jump 0 = no-op)
+        if (jump > 0) {
+            L.t += jump;
+            L.dec = false;
+        }
+        if (admit) {                                         // p = t, c = t + o (Eq. 3)
+            const int w = (int)(L.key & 63u), s = (int)((L.key >> 6) & 63u), idx = (int)(L.key >> 12);
+            L.dec = true;
+            const uint32_t S4 = rep4(s);
+            const uint32_t Kw = rep4(127 - w);
+#pragma unroll
+            for (int i = 0; i < NW; ++i)
+                L.P[i] = add_fma(L.P[i], add_fma(S4, tau_word(i)) & ~sign_bytes(Kw + tau_word(i)));
+            const int c = L.t + w;
+            if (P.start) P.start[L.off + idx] = L.t;
+            if (P.completion) P.completion[L.off + idx] = c;
+            L.sumc += c;
+            L.maxc = max(L.maxc, c);
+            if (++L.h < L.n) L.key = keys[L.off + L.h];      // the next head (used next step)
+        }
+    }
+}
+
+}  // namespace kv

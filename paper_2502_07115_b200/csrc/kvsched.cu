@@ -20,6 +20,7 @@
 #include "kernel_ring.cuh"
 #include "kernel_small.cuh"
 #include "kernel_lane.cuh"
+#include "kernel_flat.cuh"
 
 using namespace kv;
 
@@ -49,7 +50,7 @@ struct sched_ctx {
     size_t max_smem_optin = 0;
     char err[512] = {0};
     const char *last_kernel = "";
-    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk, comp;
+    DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk, comp, fkeys;
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -76,7 +77,7 @@ struct sched_ctx {
     // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
     struct RunScratch {
         cudaStream_t stream = nullptr;
-        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp;
+        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp, fkeys;
     };
     RunScratch extra[7];
     std::vector<cudaEvent_t> chunk_events;
@@ -284,6 +285,7 @@ void swap_run_scratch(sched_ctx *c, sched_ctx::RunScratch &r)
     std::swap(c->relnext, r.relnext);
     std::swap(c->retry, r.retry);
     std::swap(c->comp, r.comp);
+    std::swap(c->fkeys, r.fkeys);
 }
 
 template <typename K>
@@ -363,6 +365,32 @@ int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
     c->launches++;
     c->sim_launches++;
     c->last_kernel = name;
+    return SCHED_OK;
+}
+
+// simultaneous-arrival lane kernel: 4 warps per block, 2 KB shared memory per warp
+template <typename K>
+int launch_flat(sched_ctx *c, K kernel, const KParams &P, const char *name)
+{
+    const int block = 128, smem = 4 * 2048;
+    CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int grid = 1;
+    int rc = occupancy_grid(c, kernel, block, smem, (P.n_inst + 31) / 32, &grid);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    }
+    kernel<<<grid, block, smem, c->stream>>>(P);
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->timing) {
+        CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+        c->pending.push_back({e0, e1, name});
+    }
+    c->launches++;
+    c->sim_launches++;
     return SCHED_OK;
 }
 
@@ -531,7 +559,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             // instead of following it.  Instances the lane kernel rejects on their rows
             // (s > 7, o~ != o, gaps, invalid) are listed by it and run by k_mc_small after.
             const size_t ni = (size_t)inst->n_instances;
-            if ((rc = grow(c, c->retry, 128 + 2 * ni * 8))) return rc;
+            if ((rc = grow(c, c->retry, 128 + 3 * ni * 8))) return rc;
             unsigned long long *cnt = reinterpret_cast<unsigned long long *>(c->retry.p);
             long long *list_b = reinterpret_cast<long long *>((char *)c->retry.p + 128);
             long long *list_a = list_b + ni;
@@ -573,20 +601,44 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 return qreg ? launch_sim(c, k_mc_small<POL_MCBENCH, true, true>, Q, smem, "k_mc_small<MCBENCH>")
                             : launch_sim(c, k_mc_small<POL_MCBENCH, true, false>, Q, smem, "k_mc_small<MCBENCH,smemq>");
             };
-            // list A (size scope): beside the lane kernel on the side stream, or after it
+            // list A (size scope): beside the lane kernel on the side stream, or after it.
+            // Instances whose requests all arrive together (Arrival Model 1) run one per lane
+            // on k_mc_flat; the rest of the list goes on to k_mc_small (list C).
             KParams A = P;
             A.work_list = list_a;
             A.work_count = cnt + 1;
             A.counter = cnt + 2;
+            long long *list_c = list_a + ni;
+            const size_t key_rows = (size_t)inst->n_instances * (size_t)max_req;   // row bound
+            const bool flat = key_rows * 4 <= ((size_t)2 << 30) && !grow(c, c->fkeys, key_rows * 4 + 4);
+            auto fallback = [&]() -> int {
+                if (!flat) return small(A);
+                KParams F = A;
+                F.flat_keys = reinterpret_cast<uint32_t *>(c->fkeys.p);
+                F.retry_list = list_c;
+                F.retry_count = cnt + 6;
+                const int fnw = max_len < 16 ? 4 : max_len < 32 ? 8 : max_len < 52 ? 13 : 16;
+                int r;
+#define KV_FLAT(NWV) (sf ? launch_flat(c, k_mc_flat<POL_MCSF, NWV>, F, "k_mc_flat<MCSF>")                 \
+                         : launch_flat(c, k_mc_flat<POL_MCBENCH, NWV>, F, "k_mc_flat<MCBENCH>"))
+                r = fnw == 4 ? KV_FLAT(4) : fnw == 8 ? KV_FLAT(8) : fnw == 13 ? KV_FLAT(13) : KV_FLAT(16);
+#undef KV_FLAT
+                if (r) return r;
+                KParams C = A;
+                C.work_list = list_c;
+                C.work_count = cnt + 6;
+                C.counter = cnt + 7;
+                return small(C);
+            };
             if (side) {
                 std::swap(c->stream, c->s_side);
-                rc = cudaStreamWaitEvent(c->stream, c->ev_split, 0) == cudaSuccess ? small(A)
+                rc = cudaStreamWaitEvent(c->stream, c->ev_split, 0) == cudaSuccess ? fallback()
                          : fail(c, SCHED_E_CUDA, "cudaStreamWaitEvent failed");
                 if (!rc && cudaEventRecord(c->ev_side, c->stream) != cudaSuccess)
                     rc = fail(c, SCHED_E_CUDA, "cudaEventRecord failed");
                 std::swap(c->stream, c->s_side);
             } else {
-                rc = small(A);
+                rc = fallback();
             }
             if (rc) return rc;
             // list B (rows out of scope; usually empty): a small grid after the lane kernel
@@ -1171,7 +1223,7 @@ int sched_finalize(sched_ctx *c)
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
-        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->comp, &c->h_off,
+        for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->comp, &c->fkeys, &c->h_off,
                           &c->h_req, &c->h_mem, &c->h_out})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {
@@ -1181,7 +1233,7 @@ int sched_finalize(sched_ctx *c)
         for (auto e : c->free_events) cudaEventDestroy(e);
         for (auto e : c->chunk_events) cudaEventDestroy(e);
         for (auto &r : c->extra) {
-            for (DevBuf *b : {&r.counter, &r.bounds, &r.rq, &r.arank, &r.pstart, &r.relnext, &r.retry, &r.comp})
+            for (DevBuf *b : {&r.counter, &r.bounds, &r.rq, &r.arank, &r.pstart, &r.relnext, &r.retry, &r.comp, &r.fkeys})
                 if (b->p) cudaFree(b->p);
             if (r.stream) cudaStreamDestroy(r.stream);
         }

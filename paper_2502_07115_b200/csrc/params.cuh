@@ -39,6 +39,7 @@ struct KParams {
     unsigned long long *retry_count;
     const long long *work_list; // full-ring launch: the instances to (re)run
     const unsigned long long *work_count;
+    uint32_t *flat_keys;        // k_mc_flat: [rows] per-request keys in policy order (scratch)
 };
 
 // Lane 0 writes the per-instance outputs.

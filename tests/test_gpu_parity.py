@@ -171,6 +171,21 @@ def test_lane_kernel_scope_edges(K, ctx, oracle_mod, pol):
 
 
 @pytest.mark.parametrize("pol", [0, 1])
+def test_flat_lane_kernel(K, ctx, oracle_mod, pol):
+    """k_mc_flat: instances whose requests all arrive together (Arrival Model 1) and exceed
+    the lane kernel's 96 positions run one per lane with the queue as a rank pointer; mixed
+    with staggered large instances (k_mc_small), small ones (k_mc_lane) and invalid ones."""
+    flat = [W.am1(40, 150 + pol, n=n, M=M) for n, M in ((97, 20), (500, 40), (1000, 64), (3000, 33))]
+    paper = W.am1_paper(300, 151 + pol)                      # n 40-60 at t = 0: the lane kernel
+    stag = W.lane_mix(40, 152 + pol, n_max=400, gap_max=3)    # n > 96, not simultaneous
+    bad = W.from_instances([([[0, 9, 40, 40]] * 200, 40), ([[5, 1, 2, 2]] * 150 + [[4, 1, 2, 2]], 20)])
+    b = _concat(*flat, paper, stag, bad)
+    o, g = check(K, ctx, oracle_mod, b, pol, "flat lane kernel")
+    w = gpu_run(K, ctx, b, pol, flags=K.kvsched.FLAG_WARP_PER_INSTANCE)
+    assert_parity(o, w, b, "warp kernel")
+
+
+@pytest.mark.parametrize("pol", [0, 1])
 def test_small_kernel_large_queues(K, ctx, oracle_mod, pol):
     """More than 1024 requests per instance with M <= 64: the fused kernel keeps the waiting
     queue as a two-level shared-memory bitmap instead of one word per lane."""
