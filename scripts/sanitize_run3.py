@@ -21,6 +21,11 @@ mix = W.from_instances([b.instance(k) for k in range(50)] +
                        [([[0, 2, 3, 9], [0, 1, 5, 5]], 20), ([[3, 1, 1, 1], [2, 1, 1, 1]], 10)])
 g = K.simulate(ctx, mix, K.Policy("mcsf"), hints=K.hints_of(mix))
 print("mix", np.bincount(g["status"], minlength=4))
+for kind in ("mcsf", "mcbench"):                       # k_mc_flat (simultaneous arrivals, n > 96)
+    f = W.from_instances([W.am1(6, 9, n=300, M=40).instance(k) for k in range(6)] +
+                         [W.lane_mix(4, 3, n_max=200, gap_max=2).instance(k) for k in range(4)])
+    g = K.simulate(ctx, f, K.Policy(kind), hints=K.hints_of(f))
+    print("flat", kind, np.bincount(g["status"], minlength=4))
 c = W.am2(400, 3)
 g = K.simulate(ctx, c, K.Policy("mcsf"), hints=K.hints_of(c), packed="u8", latency16=True)
 print("u8", int(g["latency16"].max()))
