@@ -24,7 +24,7 @@ namespace kv {
 template <int NW>
 struct FlatInst {
     uint32_t P[NW];
-    uint32_t key;                // key of rank h (s, w, idx)
+    uint32_t key, key2;          // keys of ranks h and h+1 (s, w, idx): loaded two ahead
     long long inst, off, sumc, suma;
     int t, n, M, h, maxc, peak, dr, nr;
     bool active, dec;
@@ -110,10 +110,12 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         __threadfence_block();
         __syncwarp();
         const uint32_t first = keys[off];
+        const uint32_t second = n > 1 ? keys[off + 1] : 0u;
         if (lane == tl) {
 #pragma unroll
             for (int i = 0; i < NW; ++i) L.P[i] = 0u;
             L.key = first;
+            L.key2 = second;
             L.inst = inst;
             L.off = off;
             L.sumc = 0;
@@ -200,7 +202,11 @@ __global__ void __launch_bounds__(128, 4) k_mc_flat(const KParams P)
             if (P.completion) P.completion[L.off + idx] = c;
             L.sumc += c;
             L.maxc = max(L.maxc, c);
-            if (++L.h < L.n) L.key = keys[L.off + L.h];      // the next head (used next step)
+            // the next head's key was loaded a step ago; load the one after it now, so the
+            // global-memory latency hides behind a whole step
+            ++L.h;
+            L.key = L.key2;
+            if (L.h + 1 < L.n) L.key2 = keys[L.off + L.h + 1];
         }
     }
 }
