@@ -49,12 +49,36 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         bool ok = n >= 1 && n <= 32767 && M <= 64 && n <= P.max_requests && M <= P.max_mem;
         int a0 = 0;
         if (ok) {
+            // one pass: validate and (MC-SF) histogram o~; rows loaded four chunks at a time
             a0 = P.req[off].x;
+            if (POL == POL_MCSF) {
+                hist[lane] = 0;
+                hist[lane + 32] = 0;
+                __syncwarp();
+            }
             bool bad = false;
-            for (int k = lane; k < n; k += 32) {
-                const int4 r = P.req[off + k];
-                bad |= r.x != a0 || r.x < 0 || r.y < 1 || r.z < 1 || r.y + r.z > M || r.z >= 4 * NW;
-                if (POL == POL_MCSF) bad |= r.w != r.z;
+            for (int k0 = 0; k0 < n; k0 += 128) {
+                int4 r[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int k = k0 + 32 * c + lane;
+                    r[c] = k < n ? P.req[off + k] : make_int4(a0, 1, 1, 1);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int k = k0 + 32 * c + lane;
+                    if (k < n) {
+                        bad |= r[c].x != a0 || r[c].x < 0 || r[c].y < 1 || r[c].z < 1 || r[c].y + r[c].z > M ||
+                               r[c].z >= 4 * NW;
+                        if (POL == POL_MCSF) bad |= r[c].w != r[c].z;
+                    }
+                    if (POL == POL_MCSF && k0 + 32 * c < n) {
+                        const int v = k < n ? min(max(r[c].z, 0), 63) : 64 + lane;
+                        const unsigned peers = __match_any_sync(KV_FULL, v);
+                        if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                        __syncwarp();
+                    }
+                }
             }
             ok = !__any_sync(KV_FULL, bad);
         }
@@ -67,16 +91,6 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         }
         // keys in policy order: stable counting sort on o~ (MC-SF), idx order (MC-Benchmark)
         if (POL == POL_MCSF) {
-            hist[lane] = 0;
-            hist[lane + 32] = 0;
-            __syncwarp();
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                const int v = k < n ? P.req[off + k].z : 64 + lane;
-                const unsigned peers = __match_any_sync(KV_FULL, v);
-                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
-                __syncwarp();
-            }
             const int h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
             int x = h0 + h1;
 #pragma unroll
@@ -88,18 +102,27 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
             hist[2 * lane] = x - h0 - h1;
             hist[2 * lane + 1] = x - h1;
             __syncwarp();
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                const int4 r = k < n ? P.req[off + k] : make_int4(0, 0, 0, 0);
-                const int v = k < n ? r.z : 64 + lane;
-                const unsigned peers = __match_any_sync(KV_FULL, v);
-                if (k < n) {
-                    const int rk = hist[v] + __popc(peers & ((1u << lane) - 1u));
-                    keys[off + rk] = (uint32_t)r.z | ((uint32_t)r.y << 6) | ((uint32_t)k << 12);
+            for (int k0 = 0; k0 < n; k0 += 128) {
+                int4 r[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int k = k0 + 32 * c + lane;
+                    r[c] = k < n ? P.req[off + k] : make_int4(0, 0, 0, 0);
                 }
-                __syncwarp();
-                if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
-                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (k0 + 32 * c >= n) break;
+                    const int k = k0 + 32 * c + lane;
+                    const int v = k < n ? r[c].z : 64 + lane;
+                    const unsigned peers = __match_any_sync(KV_FULL, v);
+                    if (k < n) {
+                        const int rk = hist[v] + __popc(peers & ((1u << lane) - 1u));
+                        keys[off + rk] = (uint32_t)r[c].z | ((uint32_t)r[c].y << 6) | ((uint32_t)k << 12);
+                    }
+                    __syncwarp();
+                    if (k < n && __ffs(peers) - 1 == lane) hist[v] += __popc(peers);
+                    __syncwarp();
+                }
             }
         } else {
             for (int k = lane; k < n; k += 32) {
@@ -132,6 +155,51 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         }
         return true;
     }
+}
+
+// first_fit with a short dependency chain, for the latency-bound flat kernel (few lanes in
+// flight): the prefix maximum is taken inside each word first (independent across words),
+// then only the word maxima are chained (one max per word) and folded back in.
+template <int NW>
+__device__ __forceinline__ int first_fit_ll(const uint32_t (&P)[NW], int L, int w, unsigned char *fcol,
+                                            uint32_t &pk16)
+{
+    const uint32_t b64 = 0x00400040u;
+    const uint32_t kL = (uint32_t)(64 - L) * 0x00010001u;
+    uint32_t pe_l[NW], po_l[NW], mw[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const uint32_t xe = __byte_perm(P[i], 0u, 0x4240);
+        const uint32_t xo = __byte_perm(P[i], 0u, 0x4341);
+        pk16 = __vimax3_s16x2_relu(pk16, xe, xo);
+        const uint32_t te = (uint32_t)(4 * i + 1) | ((uint32_t)(4 * i + 3) << 16);
+        const uint32_t to = (uint32_t)(4 * i + 2) | ((uint32_t)(4 * i + 4) << 16);
+        const uint32_t ce = add_fma(__viaddmin_s16x2(xe, kL, b64), te);
+        const uint32_t co = add_fma(__viaddmin_s16x2(xo, kL, b64), to);
+        const uint32_t t1 = __vimax_s16x2_relu(ce, co);                       // (max c1 c2, max c3 c4)
+        po_l[i] = __vimax_s16x2_relu(t1, __byte_perm(t1, 0u, 0x1010));       // (l2, l4)
+        pe_l[i] = __vimax_s16x2_relu(ce, __byte_perm(po_l[i], 0u, 0x1044));  // (c1, max(c3, l2))
+        mw[i] = __byte_perm(po_l[i], 0u, 0x3232);                            // l4, both halves
+    }
+    uint32_t run = b64, fw[16];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        fw[i] = __byte_perm(__vimax_s16x2_relu(pe_l[i], run), __vimax_s16x2_relu(po_l[i], run), 0x6240);
+        run = __vimax_s16x2_relu(run, mw[i]);
+    }
+#pragma unroll
+    for (int i = NW; i < 16; ++i) fw[i] = 0u;
+#pragma unroll
+    for (int c = 0; c < (NW + 3) / 4; ++c)
+        *reinterpret_cast<uint4 *>(fcol + c * 512) = make_uint4(fw[4 * c], fw[4 * c + 1], fw[4 * c + 2], fw[4 * c + 3]);
+    int D = 0;
+    for (;;) {
+        const int x = min(D + w, 4 * NW) - 1;
+        const int f = (int)fcol[(x >> 4) * 512 + (x & 15)] - 64;
+        if (f <= D) break;
+        D = f;
+    }
+    return D;
 }
 
 template <int POL, int NW>
@@ -178,7 +246,7 @@ __global__ void __launch_bounds__(128, 4) k_mc_flat(const KParams P)
                 // Eq. 5 for the head at this round and, if it fails, the first round it holds;
                 // the rounds before it are decision rounds that admit nothing (no arrivals)
                 const int w = (int)(L.key & 63u), s = (int)((L.key >> 6) & 63u);
-                const int D = first_fit(L.P, L.M - s, w, fcol, pk16);
+                const int D = first_fit_ll(L.P, L.M - s, w, fcol, pk16);
                 jump = D;
                 L.dr += D;
                 admit = true;
