@@ -40,17 +40,22 @@ def gpu(ctx, b, policy, reps=3):
     ctx.run(off, req, mem, policy, out, hints=hints)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.reset_stats()
+    ctx.set_timing(True)
     e0.record()
     for _ in range(reps):
         ctx.run(off, req, mem, policy, out, hints=hints)
     e1.record()
     torch.cuda.synchronize()
+    ctx.set_timing(False)
+    kst = ctx.kernel_stats()
     ms = e0.elapsed_time(e1) / reps
     res = {k: v.cpu().numpy() for k, v in out.items()}
     res["completion"] = res["completion"][:b.n_req]
     for k in ("tel", "rounds", "decision_rounds", "evictions", "makespan", "peak_mem", "status"):
         res[k] = res[k][:b.n_inst]
-    return res, ms, ctx.last_kernel()
+    # the kernel with the most device time (a call may launch several)
+    return res, ms, max(kst, key=lambda k: kst[k][0]) if kst else ctx.last_kernel()
 
 
 def sample_parity(b, g, policy, kind, n_sample, seed=0):
