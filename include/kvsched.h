@@ -15,7 +15,10 @@
  * Policies.
  *   SCHED_MCSF        Algorithm 1: each round sort the waiting queue by o~
  *                     (ties by arrival position, DESIGN Q5) and admit the longest prefix for
- *                     which Eq. 5 holds at every future round.
+ *                     which Eq. 5 holds at every future round.  o~ > o is allowed
+ *                     (the request leaves at p + o, DESIGN Q10); for M > 64 such instances
+ *                     run on the protected kernel with alpha = 0, which gives the same
+ *                     schedule when o <= o~.
  *   SCHED_MC_BENCH    Algorithm 2: the same test in arrival order, projected
  *                     with the true o.
  *   SCHED_ALPHA       alpha-protection greedy: FCFS admission while the next-

@@ -172,7 +172,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
 
     // ---- validate (coalesced pass) ------------------------------------------------------
-    bool bad = false, unsup = n > P.max_requests || M > P.max_mem;
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem, early = false;
     long long suma = 0, sumo = 0;
     if (!unsup) {
         for (int k = lane; k < n; k += 32) {
@@ -181,7 +181,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
             if (k > 0) bad |= reqi[(off + k - 1) * 4] > r.x;
             if (POL == POL_MCSF) {
                 bad |= (long long)r.y + r.w > M || r.w < r.z;
-                unsup |= r.w != r.z;                 // early completion: small kernel only
+                early |= r.w != r.z;                 // early completion (o~ > o): k_prot
             } else {
                 bad |= (long long)r.y + r.z > M;
             }
@@ -192,6 +192,15 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     }
     bad = __any_sync(KV_FULL, bad);
     unsup = __any_sync(KV_FULL, unsup);
+    if (POL == POL_MCSF && __any_sync(KV_FULL, early) && !bad && !unsup) {
+        // MC-SF with o~ > o equals protected MC-SF with alpha = 0 (no realised overflow can
+        // occur when o <= o~): listed for the k_prot launch that follows, else UNSUPPORTED
+        if (P.early_list) {
+            if (lane == 0) P.early_list[atomicAdd(P.early_count, 1ull)] = inst;
+            return;
+        }
+        unsup = true;
+    }
     suma = warp_sum_i64(suma);
     sumo = warp_sum_i64(sumo);
     if (unsup || bad) {

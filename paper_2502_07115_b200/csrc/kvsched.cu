@@ -687,10 +687,20 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     if ((size_t)P.warp_bytes > c->max_smem_optin)
         return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
                     P.warp_bytes, P.L, P.NP);
-    if ((rc = grow(c, c->retry, 64 + (size_t)inst->n_instances * 8))) return rc;
-    P.retry_count = reinterpret_cast<unsigned long long *>(c->retry.p);
+    // retry scratch: counters {ring retry, early, k_prot retry}, then their three lists
+    const size_t ni = (size_t)inst->n_instances;
+    if ((rc = grow(c, c->retry, 64 + 3 * ni * 8))) return rc;
+    unsigned long long *rcnt = reinterpret_cast<unsigned long long *>(c->retry.p);
+    P.retry_count = rcnt;
     P.retry_list = reinterpret_cast<long long *>((char *)c->retry.p + 64);
-    CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 24, c->stream));
+    // MC-SF with early completions (o~ > o) runs on k_prot with alpha = 0 (same schedule:
+    // with o <= o~ the realised occupancy never exceeds the projection)
+    const bool early = pol->policy == SCHED_MCSF;
+    if (early) {
+        P.early_list = P.retry_list + ni;
+        P.early_count = rcnt + 1;
+    }
     // per-request scratch rows: n_instances * max_requests bounds the row count without a
     // device read; for very ragged batches that bound is loose, so read the true count
     size_t slots = (size_t)inst->n_instances * (size_t)max_req;
@@ -716,11 +726,11 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         CUDA_TRY(c, cudaGetLastError());
         c->launches++;
     }
-    if (pol->policy >= SCHED_ALPHA) {
+    if (pol->policy >= SCHED_ALPHA || early) {
         if ((rc = grow(c, c->pstart, slots * 4))) return rc;
         P.pstart = reinterpret_cast<int *>(c->pstart.p);
     }
-    if (prot) {
+    if (prot || early) {
         if ((rc = grow(c, c->relnext, slots * 4))) return rc;
         P.relnext = reinterpret_cast<int *>(c->relnext.p);
     }
@@ -750,6 +760,45 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         Q.retry_count = nullptr;
         CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
         if ((rc = launch_ring(Q))) return rc;
+    }
+    if (early) {
+        // the listed early-completion instances: k_prot (alpha = 0) over the list, with its
+        // own long-list overflow rerun at the full ring
+        const char *keep = name;
+        KParams E = P;
+        E.policy = SCHED_MCSF_PROTECTED;
+        E.alpha_num = 0;
+        E.alpha_den = 1;
+        E.early_list = nullptr;
+        E.early_count = nullptr;
+        E.work_list = P.early_list;
+        E.work_count = P.early_count;
+        E.retry_list = P.retry_list + 2 * ni;
+        E.retry_count = rcnt + 2;
+        const int Lp = L_full < KV_PROT_SHORT ? L_full : KV_PROT_SHORT;
+        E.L = Lp;
+        E.warp_bytes = prot_warp_bytes(Lp, E.NP);
+        if ((size_t)E.warp_bytes > c->max_smem_optin)
+            return fail(c, SCHED_E_ARG, "k_prot needs %d B shared memory per warp (L=%d, NP=%d)",
+                        E.warp_bytes, E.L, E.NP);
+        CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+        if ((rc = launch_sim(c, k_prot, E, E.warp_bytes, "k_prot<MCSF,early>"))) return rc;
+        if (Lp < L_full && (size_t)prot_warp_bytes(L_full, E.NP) > c->max_smem_optin) {
+            k_mark_unsupported<<<64, 128, 0, c->stream>>>(E, E.retry_list, E.retry_count);
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        } else if (Lp < L_full) {
+            KParams Q = E;
+            Q.L = L_full;
+            Q.warp_bytes = prot_warp_bytes(L_full, E.NP);
+            Q.work_list = E.retry_list;
+            Q.work_count = E.retry_count;
+            Q.retry_list = nullptr;
+            Q.retry_count = nullptr;
+            CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
+            if ((rc = launch_sim(c, k_prot, Q, Q.warp_bytes, "k_prot<MCSF,early>"))) return rc;
+        }
+        c->last_kernel = keep;
     }
     return SCHED_OK;
 }

@@ -40,6 +40,8 @@ struct KParams {
     const long long *work_list; // full-ring launch: the instances to (re)run
     const unsigned long long *work_count;
     uint32_t *flat_keys;        // k_mc_flat: [rows] per-request keys in policy order (scratch)
+    long long *early_list;      // k_ring<MCSF>: instances with o~ > o, handed to k_prot (alpha = 0)
+    unsigned long long *early_count;
 };
 
 // Lane 0 writes the per-instance outputs.

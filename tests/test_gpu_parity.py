@@ -158,6 +158,7 @@ def test_lane_kernel_scope_edges(K, ctx, oracle_mod, pol):
     big_s = W.lane_mix(300, 53, s_max=12, M_lo=20)
     gaps = W.lane_mix(300, 54, n_max=12, gap_max=900)
     edge = [([[0, 7, 57, 57]] * 96, 64), ([[0, 7, 57, 57]] * 97, 64), ([[0, 3, 5, 5]] * 128, 64),
+            ([[0, 3, 5, 5]] * 129, 64), ([[0, 8, 5, 5]] * 110, 64), ([[0, 2, 5, 5]] * 100, 64),
             ([[0, 7, 1, 1], [511, 7, 1, 1], [1022, 1, 56, 56]], 64)]
     slow = [([[0, 2, 3, 9], [0, 1, 5, 5]], 20), ([[1, 3, 4, 4], [2, 2, 2, 6]], 12)]
     bad = [([[3, 1, 1, 1], [2, 1, 1, 1]], 10), ([[0, 1, 1, 1]] * 3, 6), ([], 7), ([[0, 5, 6, 6]], 10)]
@@ -229,6 +230,41 @@ def test_prediction_overestimate_small(K, ctx, oracle_mod):
     b = W.random_small(3000, 18, n_max=50, M_lo=8, M_hi=64, a_max=40, pred_slack=8)
     assert (b.req[:, 3] > b.req[:, 2]).any()
     check(K, ctx, oracle_mod, b, 0, "o~ > o")
+
+
+def _overestimate(b, eps, seed):
+    """o~ = max(o, o^) with o^ the noisy prediction: MC-SF inputs with o~ >= o."""
+    nb = W.with_prediction_noise(b, eps, seed=seed)
+    req = nb.req.copy()
+    req[:, 3] = np.maximum(req[:, 2], req[:, 3])
+    return W.Batch(nb.offset.copy(), req, nb.mem.copy(), nb.name + "+over", dict(nb.meta))
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+@pytest.mark.parametrize("shape", ["small", "long", "c4"])
+def test_prediction_overestimate_ring(K, ctx, oracle_mod, shape, flags):
+    """MC-SF with o~ >= o on the ring path (M > 64): k_ring lists the instances with early
+    completions and k_prot runs them with alpha = 0 (the same schedule, see DESIGN Q10);
+    instances with o~ = o stay on k_ring.  Includes k_prot's long-list overflow rerun."""
+    b = {"small": lambda: W.random_small(2000, 60, n_max=40, M_lo=10, M_hi=80, a_max=30),
+         "long": lambda: _long_batch(200, 61),
+         "c4": lambda: W.c4(24, 62)}[shape]()
+    b = _overestimate(b, 0.4, 63)
+    if shape == "long":
+        many = [([[0, 1, 2100, 2107]] * 40 + [[5, 3, 50, 50], [9, 2, 2500, 2500]], 200000),
+                ([[0, 1, 3000, 3000]] * 33 + [[0, 1, 10, 12]] * 5, 120000)]
+        b = _concat(b, W.from_instances(many))
+    assert (b.req[:, 3] > b.req[:, 2]).any()
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    try:
+        o, g = check(K, ctx, oracle_mod, b, 0, f"o~ > o on the ring path ({shape})", flags=flags)
+        names = set(ctx.kernel_stats())
+    finally:
+        ctx.set_timing(False)
+        ctx.reset_stats()
+    assert "k_prot<MCSF,early>" in names and "k_ring<MCSF>" in names, names
+    assert (o["status"] == 0).sum() > 0
 
 
 @pytest.mark.parametrize("name,pol,alpha,beta", W.C4_POLICIES, ids=[p[0] for p in W.C4_POLICIES])

@@ -383,7 +383,12 @@ def test_protected_mcsf_reduces_to_mcsf(oracle_mod):
     """alpha = 0 and o^ >= o: the projection never underestimates, nothing overflows, so
     the protected variant is Algorithm 1 with o~ = o^."""
     O = oracle_mod
-    b = W.random_small(120, 91, n_max=25, M_lo=8, M_hi=60, a_max=20, pred_slack=5)
+    small = W.random_small(120, 91, n_max=25, M_lo=8, M_hi=60, a_max=20, pred_slack=5)
+    # budgets past 64 as well: the CUDA ring path runs MC-SF with o~ > o this way
+    large = W.random_small(60, 93, n_max=40, M_lo=65, M_hi=400, a_max=30, pred_slack=40)
+    insts = [small.instance(k) for k in range(small.n_inst)] + [large.instance(k) for k in range(large.n_inst)]
+    b = W.from_instances(insts)
+    assert (b.req[:, 3] > b.req[:, 2]).any() and (b.mem > 64).any()
     for k in range(b.n_inst):
         req, M = b.instance(k)
         x, y = O.simulate(req, M, O.MCSF), O.simulate(req, M, O.MCSF_PROT, alpha=(0, 1))
