@@ -738,3 +738,13 @@ def test_c4_large_every_instance(K, ctx, oracle_mod, name, pol, alpha, beta):
     polid = {"mcsf": 0, "mcbench": 1, "alpha": 2, "alpha_beta": 3}[pol]
     kw = dict(alpha=alpha or (0, 1), beta_thresh=W.beta_threshold(beta or 0.0), seed=2025)
     check(K, ctx, oracle_mod, b, polid, f"C4 10^4 {name}", **kw)
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_full_size_c2_every_instance(K, ctx, oracle_mod, pol):
+    """The bench's secondary configuration at full size (10^4 AM1 instances of 1000 requests
+    at t = 0, M = 40; k_mc_flat), every output of every instance against the oracle."""
+    b = W.am1(10_000, seed=2)
+    g = gpu_run(K, ctx, b, pol)
+    o = oracle_run(oracle_mod, b, pol)
+    assert_parity(o, g, b, f"C2 full, policy {pol}")
