@@ -158,6 +158,11 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
                     viol |= tau <= w && v + s + tau > B;
                 }
                 if (__any_sync(KV_FULL, viol)) break;
+                // the next head leaves the queue first so that its entry loads while the two
+                // ramps are written (a RETRY restarts the instance, so the order is free)
+                const int hn = q_pop_head(Q, h);
+                uint4 hen = he;
+                if (hn != KV_INF) hen = P.rq[off + hn];
                 if (!ring_admit(S.pp, mask, L, Gp, t, w, s, idx) || !ring_admit(S.pa, mask, L, Ga, t, o, s, idx)) {
                     status = ST_RETRY;
                     break;
@@ -174,9 +179,9 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
                 ++admitted;
                 ++adm_since_clear;
                 __syncwarp();
-                h = q_pop_head(Q, h);
+                h = hn;
                 if (h == KV_INF) break;
-                he = P.rq[off + h];
+                he = hen;
             }
             if (status == ST_RETRY) break;
         }
