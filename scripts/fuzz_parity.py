@@ -62,15 +62,38 @@ def main():
             hints = (0, 0, 0) if measured else K.hints_of(b)
             o = O.simulate_batch(b.offset, b.req, b.mem, pol, alpha=alpha, beta_thresh=beta, seed=seed)
             p = K.Policy(KIND[pol], alpha, beta, seed, 0, flags)
-            r = K.simulate(ctx, b, p, hints=hints)
+            # the request-row format and entry point: int32 rows on the device, a packed
+            # format when the batch encodes (decoded on the device, + latency16), or the
+            # host-buffer entry point (pipelined copies and kernels)
+            mode = str(g.choice(["i32", "u16", "u8", "p16", "host"]))
+            if mode in ("u16", "u8", "p16"):
+                pk = {"u8": b.packed_u8, "p16": b.packed_p16, "u16": b.packed_u16}[mode]()
+                if pk is None:
+                    mode = "i32"
+            if mode == "host":
+                r = {"completion": np.empty(b.n_req, np.int32), "start": np.empty(b.n_req, np.int32)}
+                for k in ("tel", "rounds", "decision_rounds", "evictions"):
+                    r[k] = np.empty(b.n_inst, np.int64)
+                for k in ("makespan", "peak_mem", "status"):
+                    r[k] = np.empty(b.n_inst, np.int32)
+                ctx.run_host(b.offset, b.req, b.mem, p, r, hints=K.hints_of(b))
+            elif mode == "i32":
+                r = K.simulate(ctx, b, p, hints=hints)
+            else:
+                r = K.simulate(ctx, b, p, hints=hints, packed=mode, latency16=True)
             bad = []
+            if "latency16" in r:
+                ok_ = np.asarray(o["status"])[np.repeat(np.arange(b.n_inst), np.diff(b.offset))] == 0
+                lat = np.minimum(np.asarray(o["completion"]).astype(np.int64) - b.req[:, 0], 65535)[ok_]
+                if not np.array_equal(np.asarray(r["latency16"]).astype(np.int64)[ok_], lat):
+                    bad.append("latency16")
             for ok, gk in FIELDS:
                 x, y = np.asarray(o[ok]).astype(np.int64), np.asarray(r[gk]).astype(np.int64)
                 if not np.array_equal(x, y):
                     bad.append(f"{ok}:{int((x != y).sum())}")
             runs += 1
             fails += bool(bad)
-            print(f"{i:4d} {shape:5s} pol={KIND[pol]:14s} alpha={alpha} flags={flags} measured_hints={measured} "
+            print(f"{i:4d} {shape:5s} {mode:4s} pol={KIND[pol]:14s} alpha={alpha} flags={flags} measured_hints={measured} "
                   f"n_inst={b.n_inst} n_req={b.n_req} -> {'OK' if not bad else 'MISMATCH ' + ' '.join(bad)}",
                   file=log, flush=True)
         print(f"runs {runs} mismatching {fails}", file=log)
