@@ -372,10 +372,13 @@ int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
 template <typename K>
 int launch_flat(sched_ctx *c, K kernel, const KParams &P, const char *name)
 {
-    const int block = 128, smem = 4 * 2048;
+    // Fewer warps than 4 per SM (C2: 10^4 lanes = 313 warps): one warp per block so the
+    // warps spread over every SM instead of packing 4 to a block on half of them.
+    const long long warps = (P.n_inst + 31) / 32;
+    const int block = warps < 4LL * c->num_sms ? 32 : 128, smem = (block / 32) * 2048;
     CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int grid = 1;
-    int rc = occupancy_grid(c, kernel, block, smem, (P.n_inst + 31) / 32, &grid);
+    int rc = occupancy_grid(c, kernel, block, smem, warps, &grid);
     if (rc) return rc;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
