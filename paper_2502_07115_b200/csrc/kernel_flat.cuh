@@ -212,12 +212,22 @@ __global__ void __launch_bounds__(128, 4) k_mc_flat(const KParams P)
     int *hist = reinterpret_cast<int *>(wbase);              // aliases F: staging only
     uint32_t *keys = P.flat_keys;                            // [rows] keys in policy order
 
+    // lanes that take instances: all 32 unless the grid has more warps than 32-lane warps
+    // need (small launches spread the instances thinner, see launch_flat)
+    uint32_t lanes = KV_FULL;
+    {
+        const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+        const long long warps_total = (long long)gridDim.x * (blockDim.x >> 5);
+        const long long lpw = (n_work + warps_total - 1) / warps_total;
+        if (lpw < 32) lanes = lpw < 1 ? 1u : (1u << lpw) - 1u;
+    }
+
     FlatInst<NW> L;
     L.active = false;
     uint32_t pk16 = 0u;
     bool more = true;
     for (;;) {
-        uint32_t idle = __ballot_sync(KV_FULL, !L.active);
+        uint32_t idle = __ballot_sync(KV_FULL, !L.active) & lanes;
         while (idle && more) {
             const int tl = __ffs(idle) - 1;
             more = flat_refill<POL, NW>(P, keys, hist, L, tl);

@@ -372,10 +372,20 @@ int launch_lane(sched_ctx *c, K kernel, const KParams &P, const char *name)
 template <typename K>
 int launch_flat(sched_ctx *c, K kernel, const KParams &P, const char *name)
 {
-    // Fewer warps than 4 per SM (C2: 10^4 lanes = 313 warps): one warp per block so the
-    // warps spread over every SM instead of packing 4 to a block on half of them.
-    const long long warps = (P.n_inst + 31) / 32;
-    const int block = warps < 4LL * c->num_sms ? 32 : 128, smem = (block / 32) * 2048;
+    // Fewer than 32 x 4 x SMs instances (C2: 10^4 = 313 full warps): one warp per block,
+    // and fewer lanes per warp (the kernel derives the count from the grid), so the launch
+    // has KV_FLAT_WARPS_PER_SM warps on every SM and each warp's divergent step is the union
+    // of fewer lanes' paths.
+#ifndef KV_FLAT_WARPS_PER_SM
+#define KV_FLAT_WARPS_PER_SM 4
+#endif
+    long long warps = (P.n_inst + 31) / 32;
+    int block = 128;
+    if (warps < (long long)KV_FLAT_WARPS_PER_SM * c->num_sms) {
+        block = 32;
+        warps = std::min<long long>(P.n_inst, (long long)KV_FLAT_WARPS_PER_SM * c->num_sms);
+    }
+    const int smem = (block / 32) * 2048;
     CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int grid = 1;
     int rc = occupancy_grid(c, kernel, block, smem, warps, &grid);
