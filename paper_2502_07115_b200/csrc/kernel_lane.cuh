@@ -322,8 +322,8 @@ __device__ __forceinline__ uint32_t max_bytes16_prefix(const uint32_t (&P)[NW], 
 // P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau).  Byte 4 NW - 1 is
 // always zero (every window ends before it), so d >= 4 NW - 1 clears the profile.  The
 // word stages are predicated moves (FMA pipe), skipped by the whole warp when no lane
-// needs them.
-template <int NW>
+// needs them (VOTE; without it every stage is predicated moves only).
+template <int NW, bool VOTE = true>
 __device__ __forceinline__ void shift_bytes(uint32_t (&P)[NW], int d)
 {
     d = min(d, 4 * NW - 1);
@@ -332,7 +332,7 @@ __device__ __forceinline__ void shift_bytes(uint32_t (&P)[NW], int d)
     for (int b = 8; b >= 1; b >>= 1) {
         if (b >= NW) continue;
         const bool on = (q & b) != 0;
-        if (__any_sync(KV_FULL, on)) {
+        if (!VOTE || __any_sync(KV_FULL, on)) {
 #pragma unroll
             for (int i = 0; i < NW; ++i)
                 if (on) P[i] = i + b < NW ? P[i + b] : 0u;
