@@ -321,8 +321,8 @@ __device__ __forceinline__ uint32_t max_bytes16_prefix(const uint32_t (&P)[NW], 
 
 // P <- P shifted down by d bytes (Prof(t+d+tau) becomes position tau).  Byte 4 NW - 1 is
 // always zero (every window ends before it), so d >= 4 NW - 1 clears the profile.  The
-// word stages are predicated moves (FMA pipe), skipped by the whole warp when no lane
-// needs them (VOTE; without it every stage is predicated moves only).
+// word stages are predicated moves (FMA pipe); with VOTE a stage is skipped by the whole
+// warp when no lane needs it (both kernels measured faster without: KV_*_SHIFT_VOTE 0).
 template <int NW, bool VOTE = true>
 __device__ __forceinline__ void shift_bytes(uint32_t (&P)[NW], int d)
 {
