@@ -270,7 +270,7 @@ def main():
     id0 = rank * batch.n_inst
     if world > 1:
         from paper_2502_07115_b200 import dist as D
-        res_dtype = D.result_dtype(batch)
+        res_dtype = D.result_dtype(batch, args.policy)
 
     # N > 1: the north star's only collective -- every rank gathers the per-instance
     # (TEL, rounds, status) of all shards and all ranks reduce the totals (NCCL over NVLink /

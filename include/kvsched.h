@@ -142,8 +142,9 @@ typedef struct {
                                    SCHED_MCSF_PROTECTED);                                   */
     int32_t alpha_den;          /*   budget B = ((den - num) * M) / den (DESIGN Q15)         */
     int32_t flags;              /* SCHED_FLAG_* bits, 0 = defaults                           */
-    uint64_t beta_thresh;       /* alpha-beta: evict iff u32 draw < beta_thresh, in [0, 2^32];
-                                   round(beta * 2^32); 2^32 = always (beta = 1)              */
+    uint64_t beta_thresh;       /* alpha-beta: evict iff u32 draw < beta_thresh, in [1, 2^32];
+                                   round(beta * 2^32); 2^32 = always (beta = 1).  At most
+                                   65536 passes per overflow, then LIVELOCK (DESIGN Q29)     */
     uint64_t seed;              /* alpha-beta RNG key                                        */
     int64_t round_cap;          /* > 0: absolute round after which the run is LIVELOCK;
                                    <= 0: min(2^30, 16 (max_a + sum_i o_i) + 64) (DESIGN Q23)  */
@@ -174,9 +175,13 @@ int sched_init(sched_ctx **out, int device, void *cuda_stream);
 /* Change the stream later calls enqueue on.                                               */
 int sched_set_stream(sched_ctx *ctx, void *cuda_stream);
 
-/* Simulate every instance of `inst` under `pol` (device pointers).  One warp per instance
- * on a persistent grid; MC policies with M <= 64 take the fused register-profile kernel,
- * everything else the shared-memory ring kernel (DESIGN "Kernels").                       */
+/* Simulate every instance of `inst` under `pol` (device pointers), on persistent grids.
+ * MC policies with M <= 64: one LANE per instance (byte-profile kernel k_mc_lane for n <= 96,
+ * k_mc_flat for larger simultaneous-arrival instances), the rest one warp per instance
+ * (k_mc_small); every other budget / policy: the shared-memory ring kernels (k_ring, k_prot)
+ * ("Kernels").  Per-instance data errors set that instance's status only.
+ * Returns SCHED_E_ARG (nothing enqueued) for bad arguments, including an unknown policy or
+ * flag, alpha outside [0, 1), or beta_thresh outside [1, 2^32] for SCHED_ALPHA_BETA.      */
 int sched_run_instances(sched_ctx *ctx, const sched_instances *inst, const sched_policy *pol,
                         const sched_outputs *out);
 

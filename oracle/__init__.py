@@ -121,7 +121,7 @@ def simulate(req, M: int, policy: int = MCSF, alpha=(0, 1), beta_thresh: int = 0
                            int(beta_thresh), int(seed) & (2**64 - 1), int(round_cap),
                            int(gid) & (2**64 - 1), _ptr(comp), _ptr(start), _ptr(st))
     if rc != 0:
-        raise ValueError("oracle: bad policy")
+        raise ValueError("oracle: bad policy (unknown id, or alpha-beta with beta_thresh 0 / > 2^32)")
     return dict(completion=comp[:n].copy(), start=start[:n].copy(), tel=int(st[0]),
                 rounds=int(st[1]), decision_rounds=int(st[2]), makespan=int(st[3]),
                 peak=int(st[4]), evictions=int(st[5]), status=int(st[6]))
@@ -142,13 +142,15 @@ def simulate_batch(offset, req, mem, policy: int = MCSF, alpha=(0, 1), beta_thre
                decision_rounds=np.zeros(max(ni, 1), np.int64),
                makespan=np.zeros(max(ni, 1), np.int32), peak=np.zeros(max(ni, 1), np.int32),
                evictions=np.zeros(max(ni, 1), np.int64), status=np.zeros(max(ni, 1), np.int32))
-    lib().or_simulate_batch(ni, _ptr(off), _ptr(r), _ptr(m), int(policy), int(alpha[0]),
+    rc = lib().or_simulate_batch(ni, _ptr(off), _ptr(r), _ptr(m), int(policy), int(alpha[0]),
                             int(alpha[1]), int(beta_thresh), int(seed) & (2**64 - 1),
                             int(round_cap), int(gid0) & (2**64 - 1), int(nthreads),
                             _ptr(out["completion"]), _ptr(out["start"]), _ptr(out["tel"]),
                             _ptr(out["rounds"]), _ptr(out["decision_rounds"]),
                             _ptr(out["makespan"]), _ptr(out["peak"]), _ptr(out["evictions"]),
                             _ptr(out["status"]))
+    if rc != 0:
+        raise ValueError("oracle: bad policy (unknown id, or alpha-beta with beta_thresh 0 / > 2^32)")
     for k in ("completion", "start"):
         out[k] = out[k][:nr]
     for k in ("tel", "rounds", "decision_rounds", "makespan", "peak", "evictions", "status"):

@@ -39,6 +39,9 @@
 #define OR_ALPHA_BETA 3  /* alpha-protection beta-clearing        */
 #define OR_MCSF_PROT 4   /* MC-SF on (1-alpha)M with clearing */
 
+/* at most this many beta passes per overflow (DESIGN Q29) */
+#define OR_BETA_MAX_PASSES 65536
+
 #define OR_OK 0
 #define OR_INVALID 1
 #define OR_LIVELOCK 2
@@ -165,6 +168,8 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
     for (int k = 0; k < 7; k++) stats[k] = 0;
     for (int64_t i = 0; i < n; i++) { completion[i] = -1; if (start) start[i] = -1; }
     if (policy < OR_MCSF || policy > OR_MCSF_PROT) return -1;
+    /* beta = beta_thresh / 2^32 must lie in (0, 1]: beta = 0 never clears (DESIGN Q29)    */
+    if (policy == OR_ALPHA_BETA && (beta_thresh == 0 || beta_thresh > (1ull << 32))) return -1;
 
     size_t nb = sizeof(int32_t) * (size_t)(n + 2);
     int32_t *a = malloc(nb), *s = malloc(nb), *o = malloc(nb), *op = malloc(nb);
@@ -278,7 +283,10 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                             evictions++;
                         }
                         nS = 0;
-                        if (have_clear && next == next_at_clear && completed_since_clear == 0) {
+                        /* DESIGN Q24: only once every request has arrived is the run from
+                         * here a repeat of the last cycle (a later arrival may sort first) */
+                        if (next == n && have_clear && next == next_at_clear &&
+                            completed_since_clear == 0) {
                             status = OR_LIVELOCK;
                             break;
                         }
@@ -286,8 +294,15 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                         next_at_clear = next;
                         completed_since_clear = 0;
                     }
-                    /* a head with s + o~ > (1-alpha)M never fits an empty worker */
-                    if (idle_before && nU == 0 && nR > 0) { status = OR_LIVELOCK; break; }
+                    /* a head with s + o~ > (1-alpha)M never fits an empty worker: nothing is
+                     * ever admitted again unless a request still to arrive sorts before it
+                     * (DESIGN Q25)                                                        */
+                    if (idle_before && nU == 0 && nR > 0) {
+                        int rescue = 0;
+                        for (int64_t j = next; j < n; j++)
+                            if (or_key_less(&I, policy, (int32_t)j, R[0])) rescue = 1;
+                        if (!rescue) { status = OR_LIVELOCK; break; }
+                    }
                 }
             } else {
                 /* alpha-protection: FCFS; admit i while the next-round occupancy
@@ -323,9 +338,11 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                         nS = 0;
                         /* "infinite processing loops": after a clear-all the state is
                          * (S empty, R, zero memory).  If nothing completed and nothing arrived
-                         * since the previous clear-all, R is the same set as then, and the
-                         * deterministic run from here repeats the last cycle for ever.      */
-                        if (have_clear && next == next_at_clear && completed_since_clear == 0) {
+                         * since the previous clear-all, R is the same set as then; once no
+                         * request is left to arrive, the deterministic run from here repeats
+                         * the last cycle for ever (DESIGN Q24).                             */
+                        if (next == n && have_clear && next == next_at_clear &&
+                            completed_since_clear == 0) {
                             status = OR_LIVELOCK;
                             break;
                         }
@@ -335,8 +352,10 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                     } else {
                         /* "each active request is cleared and sent back to the scheduler
                          * with an independent probability beta", in whole passes
-                         * until the batch fits (DESIGN Q14)                              */
-                        for (int64_t pass = 0;; pass++) {
+                         * until the batch fits (DESIGN Q14), at most OR_BETA_MAX_PASSES of
+                         * them; a batch still over M after that is LIVELOCK (DESIGN Q29)  */
+                        int64_t pass = 0;
+                        for (; pass < OR_BETA_MAX_PASSES; pass++) {
                             for (int64_t k = 0; k < nS; k++)
                                 evict[k] = (uint64_t)or_draw(seed, gid, t, pass, S[k]) < beta_thresh;
                             int64_t keep = 0;
@@ -356,6 +375,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                                 mem += (int64_t)s[S[k]] + t + 1 - p[S[k]];
                             if (mem <= M || nS == 0) break;
                         }
+                        if (pass == OR_BETA_MAX_PASSES) { status = OR_LIVELOCK; break; }
                     }
                 }
                 /* head-of-line blocked for ever: nothing was running, the FCFS head does
@@ -445,6 +465,8 @@ int or_simulate_batch(int64_t n_inst, const int64_t *offset, const int32_t *req,
                       int64_t *decision_rounds, int32_t *makespan, int32_t *peak,
                       int64_t *evictions, int32_t *status)
 {
+    if (policy < OR_MCSF || policy > OR_MCSF_PROT) return -1;
+    if (policy == OR_ALPHA_BETA && (beta_thresh == 0 || beta_thresh > (1ull << 32))) return -1;
     or_batch B = { n_inst, offset, req, mem, policy, alpha_num, alpha_den, beta_thresh, seed,
                    round_cap, gid0, completion, start, tel, rounds, decision_rounds, evictions,
                    makespan, peak, status, 0, PTHREAD_MUTEX_INITIALIZER };

@@ -9,6 +9,10 @@
 
 #define KV_FULL 0xffffffffu
 #define KV_INF 0x7fffffff
+// alpha-beta: at most this many clearing passes per overflow, then LIVELOCK (DESIGN Q29)
+#define KV_BETA_MAX_PASSES 65536
+// lane kernel scope: arrivals at most 2^29, so a run ends before the default round cap
+#define KV_LANE_MAX_A (1 << 29)
 
 namespace kv {
 

@@ -46,11 +46,16 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
         const int M = P.mem[inst];
-        bool ok = n >= 1 && n <= 32767 && M <= 64 && n <= P.max_requests && M <= P.max_mem;
+        bool ok = n >= 1 && n <= 32767 && M <= 64 && n <= P.max_requests && M <= P.max_mem &&
+                  off + n <= P.scratch_rows;
         int a0 = 0;
         if (ok) {
             // one pass: validate and (MC-SF) histogram o~; rows loaded four chunks at a time
             a0 = P.req[off].x;
+            // a run ends by a0 + sum o < a0 + 64 n: keep it below the default round cap 2^30
+            ok = (long long)a0 + 64ll * n < (1ll << 30);
+        }
+        if (ok) {
             if (POL == POL_MCSF) {
                 hist[lane] = 0;
                 hist[lane + 32] = 0;
@@ -68,8 +73,8 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
                 for (int c = 0; c < 4; ++c) {
                     const int k = k0 + 32 * c + lane;
                     if (k < n) {
-                        bad |= r[c].x != a0 || r[c].x < 0 || r[c].y < 1 || r[c].z < 1 || r[c].y + r[c].z > M ||
-                               r[c].z >= 4 * NW;
+                        bad |= r[c].x != a0 || r[c].x < 0 || r[c].y < 1 || r[c].z < 1 || r[c].w < 1 ||
+                               r[c].y + r[c].z > M || r[c].z >= 4 * NW;
                         if (POL == POL_MCSF) bad |= r[c].w != r[c].z;
                     }
                     if (POL == POL_MCSF && k0 + 32 * c < n) {

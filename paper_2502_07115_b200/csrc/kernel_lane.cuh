@@ -27,8 +27,9 @@
 // the MC-SF ranks) into the idle lane's column.
 //
 // Scope (checked per instance): 1 <= n <= 96, M <= 64, 1 <= s <= 7, o~ = o for MC-SF,
-// s + o <= M, arrivals sorted with gaps <= 511, the caller's size hints, and no user round
-// cap (MC rounds never exceed max_a + sum o, so the default cap is never reached).  Size
+// s + o <= M, arrivals sorted with gaps <= 511 and a <= 2^29, the caller's size hints, and no
+// user round cap (MC rounds never exceed max_a + sum o <= 2^29 + 95 * 511 + 96 * 63 < 2^30,
+// so the default cap min(2^30, 16 (max_a + sum o) + 64) is never reached).  Size
 // violations are listed before the launch (k_lane_split), row violations -- including
 // invalid instances, whose status the general kernel assigns -- by the kernel; k_mc_small
 // runs both lists.  Outputs are identical to k_mc_small's (and the oracle's) field by field.
@@ -189,8 +190,10 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
                 if (lane == 31) nx = nx0;
                 an[c] = (k + 1 < n) ? nx - r[c].x : 0;           // a_(k+1) - a_k
                 if (k < n) {
-                    bad |= r[c].x < 0 || r[c].y < 1 || r[c].y > 7 || r[c].z < 1 || r[c].y + r[c].z > M ||
-                           r[c].z >= 4 * NW;               // window within the profile words
+                    bad |= r[c].x < 0 || r[c].y < 1 || r[c].y > 7 || r[c].z < 1 || r[c].w < 1 ||
+                           r[c].y + r[c].z > M ||
+                           r[c].z >= 4 * NW ||             // window within the profile words
+                           r[c].x > KV_LANE_MAX_A;         // the default round cap stays out of reach
                     if (POL == POL_MCSF) bad |= r[c].w != r[c].z;
                     bad |= an[c] < 0 || an[c] > 511;
                     suma += r[c].x;

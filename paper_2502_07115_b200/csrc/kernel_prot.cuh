@@ -43,7 +43,7 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
     const int *reqi = reinterpret_cast<const int *>(P.req);
     InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
 
-    bool bad = false, unsup = n > P.max_requests || M > P.max_mem;
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows;
     long long suma = 0, sumo = 0;
     if (!unsup) {
         for (int k = lane; k < n; k += 32) {
@@ -224,12 +224,21 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
             Ga.used = 0u;
             __syncwarp();
             evictions += ev;
-            cycle = next_at_clear == next && ev == adm_since_clear;
+            cycle = next == n && next_at_clear == next && ev == adm_since_clear;
             next_at_clear = next;
             adm_since_clear = 0;
         }
         if (cycle) { status = ST_LIVELOCK; break; }
-        if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
+        if (idle_before && admitted == 0 && h != KV_INF) {
+            // S empty and the head does not fit an empty worker (s + o~ > (1-alpha)M): stuck
+            // for ever unless a request still to arrive sorts before it (DESIGN Q25)
+            bool rescue = false;
+            for (int k = next; k < n && !rescue; k += 32) {
+                const int kk = k + lane;
+                rescue = __any_sync(KV_FULL, kk < n && P.arank[off + kk] < h);
+            }
+            if (!rescue) { status = ST_LIVELOCK; break; }
+        }
         if (had_R || !idle_before) ++rounds;
         const int mnow = ring_jump(S.pa, mask, L, Ga, t, t + 1, t + 1);   // Mem(t+1)
         ring_jump(S.pp, mask, L, Gp, t, t, t + 1);

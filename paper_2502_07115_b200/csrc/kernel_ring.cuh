@@ -172,7 +172,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
 
     // ---- validate (coalesced pass) ------------------------------------------------------
-    bool bad = false, unsup = n > P.max_requests || M > P.max_mem, early = false;
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows, early = false;
     long long suma = 0, sumo = 0;
     if (!unsup) {
         for (int k = lane; k < n; k += 32) {
@@ -239,7 +239,8 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
     int mem_prev = 0;                    // alpha: Mem(t) of the previous round
     // alpha-greedy cycle detection (DESIGN Q24): admissions since the last clear-all and the
     // arrival pointer then; a clear-all that evicts everything admitted since the previous
-    // one (nothing completed) with no arrival in between repeats that cycle for ever.
+    // one (nothing completed), with no arrival in between and none left to come, repeats
+    // that cycle for ever.
     int adm_since_clear = 0, next_at_clear = -1;
     LongList G;
     G.p = G.s = G.e = G.idx = 0;
@@ -406,7 +407,9 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
             // overflow of the batch of round t (DESIGN Q13): clear or thin
             const int *pst = P.pstart;
             const long long ev_before = evictions;
-            for (int pass = 0;; ++pass) {
+            int pass = 0;
+            for (;; ++pass) {
+                if (pass == KV_BETA_MAX_PASSES) { status = ST_LIVELOCK; break; }   // DESIGN Q29
                 int left = 0;
                 for (int wb = 0; wb < nw; wb += 32) {
                     const int wi = wb + lane;
@@ -464,7 +467,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                     __syncwarp();
                     G.used = 0u;
                     mem = 0;
-                    cycle = next_at_clear == next && evictions - ev_before == adm_since_clear;
+                    cycle = next == n && next_at_clear == next && evictions - ev_before == adm_since_clear;
                     next_at_clear = next;
                     adm_since_clear = 0;
                     break;
@@ -473,7 +476,7 @@ __device__ void ring_instance(const KParams &P, long long inst, const RingSmem &
                 if (mem <= M || left == 0) break;
             }
         }
-        if (cycle) { status = ST_LIVELOCK; break; }
+        if (cycle || status == ST_LIVELOCK) { status = ST_LIVELOCK; break; }
         if (idle_before && admitted == 0 && h != KV_INF) { status = ST_LIVELOCK; break; }
         if (had_R || !idle_before) ++rounds;
         __syncwarp();
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(1024) k_rank_sort(const KParams P, uint4 *rq, 
     for (long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
-        if (n <= 0 || n > P.max_requests) continue;
+        if (n <= 0 || n > P.max_requests || off + n > P.scratch_rows) continue;
         const int NPi = next_pow2(n);
         for (int k = threadIdx.x; k < NPi; k += blockDim.x) {
             uint32_t key = 0xffffffffu;

@@ -439,6 +439,8 @@ int check_policy(sched_ctx *c, const sched_policy *pol)
         if (pol->alpha_den <= 0 || pol->alpha_num < 0 || pol->alpha_num >= pol->alpha_den)
             return fail(c, SCHED_E_ARG, "alpha = %d/%d must lie in [0, 1)", pol->alpha_num, pol->alpha_den);
         if (pol->beta_thresh > (1ull << 32)) return fail(c, SCHED_E_ARG, "beta_thresh must be <= 2^32");
+        if (pol->policy == SCHED_ALPHA_BETA && pol->beta_thresh == 0)
+            return fail(c, SCHED_E_ARG, "alpha-beta needs beta_thresh >= 1 (beta = 0 never clears)");
     }
     return SCHED_OK;
 }
@@ -553,6 +555,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     P.peak = out->peak_mem;
     P.status = out->status;
     P.counter = reinterpret_cast<unsigned long long *>(c->counter.p);
+    P.scratch_rows = 0x7fffffffffffffffll;            // set below where scratch is sized
     CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
 
     const bool mc = pol->policy == SCHED_MCSF || pol->policy == SCHED_MC_BENCH;
@@ -628,6 +631,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 if (!flat) return small(A);
                 KParams F = A;
                 F.flat_keys = reinterpret_cast<uint32_t *>(c->fkeys.p);
+                F.scratch_rows = (long long)key_rows;
                 F.retry_list = list_c;
                 F.retry_count = cnt + 6;
                 const int fnw = max_len < 16 ? 4 : max_len < 32 ? 8 : max_len < 52 ? 13 : 16;
@@ -726,6 +730,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         if (rows < slots) slots = rows;
     }
     const char *name = "";
+    P.scratch_rows = (long long)slots;
     if (pol->policy == SCHED_MCSF || prot) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
         // offsets are relative to the batch: scratch slot = request row (n_req <= slots)

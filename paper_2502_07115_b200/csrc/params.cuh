@@ -42,6 +42,10 @@ struct KParams {
     uint32_t *flat_keys;        // k_mc_flat: [rows] per-request keys in policy order (scratch)
     long long *early_list;      // k_ring<MCSF>: instances with o~ > o, handed to k_prot (alpha = 0)
     unsigned long long *early_count;
+    // rows of the per-request scratch above (sized from the max_requests hint); an instance
+    // whose rows fall past it (only possible after an instance that broke the caller's
+    // hint) is UNSUPPORTED instead of writing out of bounds
+    long long scratch_rows;
 };
 
 // Lane 0 writes the per-instance outputs.

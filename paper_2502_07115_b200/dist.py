@@ -38,10 +38,16 @@ def shard_bounds(n_total: int, world: int, rank: int, weights=None) -> tuple[int
     return cut(rank), cut(rank + 1)
 
 
-def result_dtype(batch) -> torch.dtype:
-    """int32 rows when every TEL and round count provably fits (TEL <= n (max_a + sum o),
-    the MC bound; the alpha policies' LIVELOCK instances report -1), else int64.  Halves
-    the bytes the gather moves on the bench workloads."""
+def result_dtype(batch, policy: str = "mcsf", round_cap: int = 0) -> torch.dtype:
+    """int32 rows when every TEL and round count provably fits, else int64.  Halves the bytes
+    the gather moves on the bench workloads.
+
+    Bounds (per instance, n requests, c_i the completion of an OK run):
+      MC-SF / MC-Benchmark: every round with S empty admits the head, so c_i <= max_a + sum o
+        and TEL <= n (max_a + sum o);
+      evicting policies (alpha, alpha-beta, protected MC-SF): a run can last until the round
+        cap, so c_i <= cap + max o <= cap + sum o, cap = round_cap if > 0 else the default
+        min(2^30, 16 (max_a + sum o) + 64) (DESIGN Q23), and TEL <= n (cap + sum o)."""
     import numpy as np
     if batch.n_inst == 0 or batch.n_req == 0:
         return torch.int32
@@ -50,7 +56,13 @@ def result_dtype(batch) -> torch.dtype:
     amax = np.where(sizes > 0, batch.req[np.maximum(last, 0), 0].astype(np.int64), 0)
     sumo = np.add.reduceat(batch.req[:, 2].astype(np.int64), np.minimum(batch.offset[:-1], batch.n_req - 1))
     sumo = np.where(sizes > 0, sumo, 0)
-    bound = int((sizes * (amax + sumo)).max(initial=0))
+    if policy in ("mcsf", "mcbench"):
+        horizon = amax + sumo
+    else:
+        cap = np.full_like(amax, int(round_cap)) if round_cap > 0 else \
+            np.minimum(16 * (amax + sumo) + 64, 2 ** 30)
+        horizon = cap + sumo
+    bound = int((sizes * horizon).max(initial=0))
     return torch.int32 if bound < 2**31 - 1 else torch.int64
 
 

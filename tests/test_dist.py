@@ -89,3 +89,10 @@ def test_result_dtype_bound():
     big = W.from_instances([([[0, 1, 30000, 30000]] * 80000, 2**20)])
     assert D.result_dtype(big) == torch.int64
     assert D.result_dtype(W.from_instances([([], 7)])) == torch.int32
+    # MC bound n (max_a + sum o) = 2000 * 1e6 fits int32; an evicting policy may run to the
+    # round cap 16x later, whose bound does not (no silent wrap in the gather)
+    mid = W.from_instances([([[0, 1, 500, 500]] * 2000, 1002)])
+    assert D.result_dtype(mid, "mcsf") == torch.int32
+    for pol in ("alpha", "alpha_beta", "mcsf_protected"):
+        assert D.result_dtype(mid, pol) == torch.int64
+    assert D.result_dtype(mid, "alpha", round_cap=1000) == torch.int32

@@ -748,3 +748,102 @@ def test_full_size_c2_every_instance(K, ctx, oracle_mod, pol):
     g = gpu_run(K, ctx, b, pol)
     o = oracle_run(oracle_mod, b, pol)
     assert_parity(o, g, b, f"C2 full, policy {pol}")
+
+
+# ---------------------------------------------------------------------------------------
+# Round 2: the cycle rule only once nothing is left to arrive (DESIGN Q24/Q25), the beta
+# pass cap and beta = 0 rejection (Q29), the hand-worked eviction cases
+# ---------------------------------------------------------------------------------------
+R2 = json.loads((GOLDEN / "round2_pins.json").read_text())
+
+
+@pytest.mark.parametrize("case", R2["cases"], ids=lambda c: c["name"])
+def test_round2_worked_examples_on_gpu(K, ctx, oracle_mod, case):
+    pol = {"alpha": 2, "alpha_beta": 3, "mcsf_prot": 4}[case["policy"]]
+    b = W.from_instances([(case["req"], case["M"])])
+    o, g = check(K, ctx, oracle_mod, b, pol, case["name"], alpha=tuple(case["alpha"]),
+                 beta_thresh=case.get("beta_thresh", 0), seed=case.get("seed", 0),
+                 id0=case.get("gid", 0))
+    for k, v in case["expect"].items():
+        gk = "peak_mem" if k == "peak" else k
+        got = g[gk] if k in ("completion", "start") else g[gk][0]
+        assert (list(got) == v) if isinstance(v, list) else (got == v), (k, got, v)
+
+
+@pytest.mark.parametrize("pol", [2, 3, 4])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_cycles_meeting_arrivals(K, ctx, oracle_mod, pol, flags):
+    """Staggered arrivals into tight budgets: evictions cycle while requests are still to
+    arrive, so the cycle rule must wait for the last arrival (both sides)."""
+    b = W.random_small(4000, 130 + pol, n_max=12, M_lo=6, M_hi=40, a_max=80)
+    kw = dict(alpha=(1, 10))
+    if pol == 3:
+        kw.update(beta_thresh=W.beta_threshold(0.2), seed=17)
+    if pol == 4:
+        b = W.with_prediction_noise(b, 0.8, seed=12)
+        kw = dict(alpha=(0, 1))
+    o, _ = check(K, ctx, oracle_mod, b, pol, f"cycles pol={pol}", flags=flags, **kw)
+    assert o["evictions"].sum() > 0
+    if pol != 3:
+        assert (o["status"] == 2).any()
+
+
+def test_alpha_beta_pass_cap_and_zero_beta(K, ctx, oracle_mod):
+    """beta_thresh = 1: 65536 passes evict nobody at E9's overflow -> LIVELOCK on both sides;
+    beta_thresh = 0 is refused by the ABI before anything is enqueued."""
+    b = W.from_instances([([[0, 1, 40, 40], [0, 1, 40, 40]], 50), ([[0, 1, 3, 3]] * 3, 8)])
+    o, g = check(K, ctx, oracle_mod, b, 3, "pass cap", alpha=(3, 10), beta_thresh=1, seed=3)
+    assert list(g["status"]) == [2, 0]
+    with pytest.raises(Exception):
+        gpu_run(K, ctx, b, 3, alpha=(3, 10), beta_thresh=0)
+
+
+@pytest.mark.parametrize("pol", [0, 1])
+def test_zero_prediction_is_invalid_on_every_kernel(K, ctx, oracle_mod, pol):
+    """o~ < 1 is INVALID for every policy (DESIGN Q8), whichever kernel picks the instance up:
+    k_mc_lane (n <= 96), k_mc_flat (simultaneous, n > 96), k_mc_small, k_ring (M > 64)."""
+    row0 = [0, 2, 3, 0]
+    insts = [([row0, [0, 1, 3, 3]], 10),                                   # lane
+             ([row0] + [[0, 1, 2, 2]] * 120, 40),                          # flat
+             ([[0, 1, 2, 2]] * 100 + [[1, 1, 2, 0]], 40),                  # small
+             ([row0, [3, 1, 3, 3]], 300),                                  # ring
+             ([[0, 1, 3, 3], [0, 2, 4, 4]], 10)]                           # valid
+    b = W.from_instances(insts)
+    o, g = check(K, ctx, oracle_mod, b, pol, "o~ = 0")
+    assert list(g["status"]) == [1, 1, 1, 1, 0]
+
+
+@pytest.mark.parametrize("pol", [0, 1, 2, 4])
+def test_hint_violation_does_not_spill_scratch(K, ctx, oracle_mod, pol):
+    """An instance larger than the caller's max_requests hint comes first, so every later
+    instance's rows lie past n_instances * hint.  The violator is UNSUPPORTED; later instances
+    are either exact or UNSUPPORTED (their scratch rows would fall outside the allocation) --
+    never written out of bounds (compute-sanitizer runs cover the same batch)."""
+    big = ([[0, 1, 5, 5]] * 400, 300)
+    rest = W.random_small(60, 27, n_max=15, M_lo=70, M_hi=200, a_max=20)
+    insts = [big] + [rest.instance(k) for k in range(rest.n_inst)]
+    b = W.from_instances(insts)
+    kw = dict(alpha=(1, 10)) if pol >= 2 else {}
+    g = gpu_run(K, ctx, b, pol, hints=(20, 300, 63), **kw)
+    o = oracle_run(oracle_mod, b, pol, **kw)
+    assert g["status"][0] == 3
+    for k in range(1, b.n_inst):
+        if g["status"][k] == 3:
+            continue
+        lo, hi = b.offset[k], b.offset[k + 1]
+        assert g["status"][k] == o["status"][k] and g["tel"][k] == o["tel"][k], k
+        assert np.array_equal(g["completion"][lo:hi], o["completion"][lo:hi]), k
+
+
+def test_lane_scope_far_arrivals(K, ctx, oracle_mod):
+    """Arrival rounds near 2^30: the default cap min(2^30, ...) is reachable, so the lane and
+    flat kernels must hand such instances to the general kernel."""
+    base = 2**30 - 40
+    insts = [([[base, 1, 30, 30], [base, 1, 30, 30]], 40),
+             ([[base + 5, 2, 10, 10]] * 3, 30),
+             ([[2**29 + 1, 1, 4, 4]], 10),
+             ([[base, 1, 20, 20]] * 120, 41),
+             ([[0, 1, 4, 4]], 10)]
+    b = W.from_instances(insts)
+    for pol in (0, 1):
+        check(K, ctx, oracle_mod, b, pol, "far arrivals")

@@ -476,3 +476,139 @@ def test_wallclock_unit_clock_is_tel(oracle_mod):
         assert w["mem"].max() == out["peak"]
         w2 = O.wallclock(req, out["start"], out["completion"], 3, 1, 7, 10_000, 0)
         assert w2["bins"].sum() == int((req[:, 1] + req[:, 2] - 1).sum())
+
+
+# ----------------------------------------------------------------------------------------
+# Round 2: eviction policies against hand-worked cases and an independent literal re-run
+# ----------------------------------------------------------------------------------------
+R2 = json.loads((GOLDEN / "round2_pins.json").read_text())
+POL2 = dict(POL, mcsf_prot=4)
+
+
+@pytest.mark.parametrize("case", R2["cases"], ids=lambda c: c["name"])
+def test_round2_worked_examples(oracle_mod, case):
+    O = oracle_mod
+    out = O.simulate(case["req"], case["M"], POL2[case["policy"]], alpha=tuple(case["alpha"]),
+                     beta_thresh=case.get("beta_thresh", 0), seed=case.get("seed", 0),
+                     gid=case.get("gid", 0))
+    for k, v in case["expect"].items():
+        got = list(out[k]) if isinstance(v, list) else out[k]
+        assert got == v, (k, got, v)
+
+
+def test_round2_beta_draws_are_philox(oracle_mod):
+    """The draws written into the alpha-beta pin (computed with workloads' numpy Philox) are
+    what the oracle's Philox gives on counter (t, pass, idx, 0) and key = seed halves (gid 0)."""
+    case = next(c for c in R2["cases"] if c["policy"] == "alpha_beta")
+    seed, t = case["seed"], case["draws"]["t"]
+    for p, row in enumerate(case["draws"]["by_pass"]):
+        for idx, hx in enumerate(row):
+            got = oracle_mod.philox4x32_10([t, p, idx, 0], [seed & 0xFFFFFFFF, seed >> 32])[0]
+            assert got == int(hx, 16)
+            ref = W._philox_np([t], [p], [idx], [0], [seed & 0xFFFFFFFF], [seed >> 32])[0][0]
+            assert int(ref) == int(hx, 16)
+
+
+@pytest.mark.parametrize("case", R2["tel"], ids=lambda c: c["name"])
+def test_or_tel_pins(oracle_mod, case):
+    req = np.asarray(case["req"], np.int32).reshape(-1, 4)
+    assert oracle_mod.tel(req, np.asarray(case["completion"], np.int32)) == case["tel"]
+
+
+def test_alpha_beta_rejects_beta_zero_and_caps_passes(oracle_mod):
+    """beta = 0 never clears (DESIGN Q29): refused.  A tiny beta (threshold 1 of 2^32) on the
+    E9 overflow: 65536 passes evict nobody, so the run ends LIVELOCK at that overflow (t=24)."""
+    O = oracle_mod
+    e9 = [[0, 1, 40, 40], [0, 1, 40, 40]]
+    with pytest.raises(ValueError):
+        O.simulate(e9, 50, 3, alpha=(3, 10), beta_thresh=0)
+    with pytest.raises(ValueError):
+        O.simulate_batch([0, 2], e9, [50], 3, alpha=(3, 10), beta_thresh=0)
+    with pytest.raises(ValueError):
+        O.simulate(e9, 50, 3, alpha=(3, 10), beta_thresh=2**32 + 1)
+    out = O.simulate(e9, 50, 3, alpha=(3, 10), beta_thresh=1, seed=3)
+    assert out["status"] == 2 and out["evictions"] == 0 and out["decision_rounds"] == 1
+
+
+def _literal_rerun(req, M, policy, alpha, cap):
+    """An independent, literal re-run of alpha-greedy or protected MC-SF
+     written from the paper's rules, with NO cycle detection: it stops only when
+    every request has completed or at the round cap.  Returns (completion, finished)."""
+    req = np.asarray(req, np.int64)
+    n = len(req)
+    a, s, o, op = (req[:, k] for k in range(4))
+    B = ((alpha[1] - alpha[0]) * M) // alpha[1]
+    p = [-1] * n
+    c = [-1] * n
+    R, S = [], []
+    t, nxt = int(a[0]), 0
+    while t <= cap:
+        while nxt < n and a[nxt] <= t:
+            R.append(nxt)
+            nxt += 1
+        S = [j for j in S if c[j] > t]
+        if policy == 2:
+            R.sort()
+            L = sum(int(s[j]) + t + 1 - p[j] for j in S)
+            while R and L + s[R[0]] + 1 <= B:
+                i = R.pop(0)
+                L += int(s[i]) + 1
+                p[i], c[i] = t, t + int(o[i])
+                S.append(i)
+        else:
+            R.sort(key=lambda i: (op[i], i))
+            U = []
+            for i in list(R):
+                ok = True
+                for tp in range(t + 1, t + max(int(op[k]) for k in U + [i]) + 1):
+                    load = sum(int(s[j]) + tp - p[j] for j in S if op[j] >= tp - p[j])
+                    load += sum(int(s[k]) + tp - t for k in U + [i] if op[k] >= tp - t)
+                    if load > B:
+                        ok = False
+                        break
+                if not ok:
+                    break
+                U.append(i)
+            for i in U:
+                R.remove(i)
+                p[i], c[i] = t, t + int(o[i])
+                S.append(i)
+        if sum(int(s[j]) + t + 1 - p[j] for j in S) > M:
+            for j in S:
+                p[j] = c[j] = -1
+                R.append(j)
+            S = []
+        if nxt == n and not R and not S:
+            return c, True
+        if not R and not S:
+            t = int(a[nxt])
+        else:
+            t += 1
+    return c, False
+
+
+@pytest.mark.parametrize("policy", [2, 4])
+def test_cycle_rule_matches_round_capped_rerun(oracle_mod, policy):
+    """DESIGN Q24/Q25: declaring LIVELOCK early never changes a completion or the status
+    against a literal run to the round cap (staggered arrivals, so cycles meet arrivals)."""
+    O = oracle_mod
+    b = W.random_small(400, 123 + policy, n_max=6, M_lo=6, M_hi=20, a_max=40)
+    if policy == 4:
+        b = W.with_prediction_noise(b, 0.8, seed=11)
+    alpha = (1, 10) if policy == 2 else (0, 1)
+    n_live = 0
+    for k in range(b.n_inst):
+        req, M = b.instance(k)
+        if len(req) == 0:
+            continue
+        out = O.simulate(req, M, policy, alpha=alpha)
+        if out["status"] == 1:
+            continue
+        cap = 16 * (int(req[-1, 0]) + int(req[:, 2].sum())) + 64
+        comp, done = _literal_rerun(req, M, policy, alpha, cap)
+        assert (out["status"] == 0) == done, (k, out["status"])
+        # a request still in flight when the cap stops a run has not completed
+        norm = lambda cs: [int(x) if x <= cap else -1 for x in cs]
+        assert norm(out["completion"]) == norm(comp), k
+        n_live += out["status"] == 2
+    assert n_live > 0
