@@ -45,7 +45,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kvsched", choices=["kvsched", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4", "c3"])
-    ap.add_argument("--instances", type=int, default=0, help="instances per GPU (0 = config size)")
+    ap.add_argument("--instances", type=int, default=0,
+                    help="instances (0 = config size): of the whole job with --split strong, per GPU with weak")
+    ap.add_argument("--split", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's batch (C5: 10^6 instances) is cut across the "
+                         "ranks by dist.shard_bounds, balanced by request count; weak: every rank "
+                         "runs its own full-size batch")
+    ap.add_argument("--dump-results", default="",
+                    help="rank 0 saves the gathered per-instance (TEL, rounds, status) rows of the "
+                         "last step here (.npy; tests compare 1-rank and N-rank runs)")
     ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta", "mcsf_protected"])
     ap.add_argument("--eps", type=float, default=0.2, help="prediction noise for mcsf_protected (P:519)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -59,7 +67,29 @@ def parse():
     return ap.parse_args()
 
 
-def make_workload(name: str, n: int, rank: int):
+def make_workload(name: str, n: int, rank: int, world: int = 1, split: str = "weak"):
+    """The config's synthetic batch for this rank and the instance id of its first instance.
+
+    split == "strong": every rank draws the same global batch (rank 0's seed) and keeps the
+    contiguous shard [lo, hi) of dist.shard_bounds weighted by request count; its instance
+    ids are lo..hi-1, so the alpha-beta RNG and every output equal the 1-GPU run's.
+    split == "weak": rank r draws its own full-size batch (ids r*n ...)."""
+    if split == "strong" and world > 1:
+        from paper_2502_07115_b200 import dist as D
+        full, cfg = make_workload(name, n, 0)
+        full = full[0]
+        bounds = [D.shard_bounds(full.n_inst, world, r, weights=full.sizes()) for r in range(world)]
+        lo, hi = bounds[rank]
+        cfg.pop("instances_per_gpu", None)
+        cfg.update(instances_total_config=full.n_inst, shard=[lo, hi], split="strong",
+                   shard_sizes=[b - a for a, b in bounds])
+        return (full.slice(lo, hi), lo), cfg
+    b, cfg = _make_workload(name, n, rank)
+    cfg.update(split=split if world > 1 else "single", shard_sizes=[b.n_inst] * world)
+    return (b, rank * b.n_inst), cfg
+
+
+def _make_workload(name: str, n: int, rank: int):
     if name == "c5":
         n = n or 1_000_000
         return W.am2(n, seed=5, id0=rank * n), dict(workload="C5 AM2 sweep lambda{0.5..1.5} x M{30..50}",
@@ -209,7 +239,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    batch, cfg = make_workload(args.workload, args.instances, 0)
+    (batch, _), cfg = make_workload(args.workload, args.instances, 0)
     if args.policy == "mcsf_protected":
         batch = W.with_prediction_noise(batch, args.eps, seed=7)
         cfg["prediction_noise_eps"] = args.eps
@@ -256,7 +286,7 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    batch, cfg = make_workload(args.workload, args.instances, rank)
+    (batch, id0), cfg = make_workload(args.workload, args.instances, rank, world, args.split)
     if args.policy == "mcsf_protected":
         batch = W.with_prediction_noise(batch, args.eps, seed=7 + rank)
         cfg["prediction_noise_eps"] = args.eps
@@ -267,10 +297,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ctx = K.Context(local, stream=stream.cuda_stream)
     pol = policy_of(K, args.policy)
-    id0 = rank * batch.n_inst
+    shard_sizes = cfg.pop("shard_sizes")
     if world > 1:
         from paper_2502_07115_b200 import dist as D
         res_dtype = D.result_dtype(batch, args.policy)
+        # the gather pads every shard to the largest one (strong split: shards differ by a few)
+        n_pad = max(shard_sizes)
+        gathered = [None, None]
 
     # N > 1: the north star's only collective -- every rank gathers the per-instance
     # (TEL, rounds, status) of all shards and all ranks reduce the totals (NCCL over NVLink /
@@ -291,13 +324,13 @@ def main():
             nstep[0] += 1
             if done_ev[j] is not None:
                 stream.wait_event(done_ev[j])
-            packed[j] = D.pack_results(out, batch.n_inst, batch.n_inst, dev, res_dtype)
+            packed[j] = D.pack_results(out, batch.n_inst, n_pad, dev, res_dtype)
             ready = torch.cuda.Event()
             ready.record(stream)
             packed[j].record_stream(coll)               # allocator: in use on the side stream
             with torch.cuda.stream(coll):
                 coll.wait_event(ready)
-                D.gather_results(packed[j])
+                gathered[j] = D.gather_results(packed[j])
                 D.reduce_totals({k: packed[j][i] for i, k in enumerate(D.RESULT_ROWS)}, batch.n_inst)
                 done_ev[j] = torch.cuda.Event()
                 done_ev[j].record(coll)
@@ -472,12 +505,12 @@ def main():
     # protocol, reported beside the primary workload
     also = None
     if not args.no_also and args.workload == "c5" and args.policy == "mcsf":
-        b2, cfg2 = make_workload("c2", 0, rank)
+        (b2, id2), cfg2 = make_workload("c2", 0, rank, world, args.split)
         o2, r2, m2 = K.to_device(b2, dev)
         out2 = K.alloc_outputs(b2.n_inst, b2.n_req, dev, fields)
         h2 = K.hints_of(b2)
         for _ in range(max(args.warmup, 1)):
-            ctx.run(o2, r2, m2, pol, out2, id0=rank * b2.n_inst, hints=h2)
+            ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
         torch.cuda.synchronize(dev)
         rounds2 = int(out2["rounds"][:b2.n_inst].clamp(min=0).sum().item())
         if world > 1:
@@ -487,7 +520,7 @@ def main():
         ctx.set_timing(True)
         h0.record(stream)
         for _ in range(args.steps):
-            ctx.run(o2, r2, m2, pol, out2, id0=rank * b2.n_inst, hints=h2)
+            ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
         h1.record(stream)
         torch.cuda.synchronize(dev)
         t2 = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
@@ -505,8 +538,18 @@ def main():
                        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kst2.items()}}}
         del o2, r2, m2, out2
 
+    # rank 0: the gathered per-instance rows of the last timed step, in global instance order
+    if args.dump_results and rank == 0:
+        if world > 1:
+            rows = D.unpad(gathered[(nstep[0] - 1) % 2], shard_sizes).to(torch.int64).cpu().numpy()
+        else:
+            rows = np.stack([out[k][:batch.n_inst].to(torch.int64).cpu().numpy() for k in ("tel", "rounds", "status")])
+        np.save(args.dump_results, rows)
+
+    # the oracle on rank 0's host cores, over a bounded prefix of rank 0's shard (at N > 1
+    # the other ranks wait at the final barrier; the timed region is over)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(batch, args.policy, args.cpu_seconds, gid0=id0)
         one = cpu_oracle_rate(batch, args.policy, min(3.0, args.cpu_seconds / 4), gid0=id0, nthreads=1)
         cpu["single_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
@@ -518,7 +561,8 @@ def main():
                    generator=W.GENERATOR_VERSION)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "scaling": args.split,
+                "vs_baseline": None, "dtype": "int32", "data": "synthetic",
                 "config": cfg, "instances_per_s": inst_all * args.steps / (ms_max / 1000.0),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
                 "gpu_launches": st["launches"], "decision_rounds_per_step": drounds_rank * world,
@@ -526,6 +570,7 @@ def main():
         print(json.dumps(line))
     ctx.close()
     if world > 1:
+        dist.barrier()                  # rank 0 may still be timing the oracle
         dist.destroy_process_group()
     return 0
 

@@ -80,6 +80,10 @@ def gather_results(local: torch.Tensor, group=None) -> torch.Tensor:
     out = torch.empty((world, *local.shape), dtype=local.dtype, device=local.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    elif local.is_cuda:                 # gloo: through host memory (multi-rank tests on one GPU)
+        parts = [torch.empty(local.shape, dtype=local.dtype) for _ in range(world)]
+        dist.all_gather(parts, local.cpu().contiguous(), group=group)
+        out.copy_(torch.stack(parts))
     else:
         dist.all_gather(list(out.unbind(0)), local.contiguous(), group=group)
     return out

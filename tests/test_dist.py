@@ -96,3 +96,22 @@ def test_result_dtype_bound():
     for pol in ("alpha", "alpha_beta", "mcsf_protected"):
         assert D.result_dtype(mid, pol) == torch.int64
     assert D.result_dtype(mid, "alpha", round_cap=1000) == torch.int32
+
+
+def test_bench_strong_split_partitions_the_config_batch():
+    """bench.make_workload(split="strong"): the shards of ranks 0..W-1 are contiguous,
+    cover the config's batch exactly once, carry their global first id, and are balanced by
+    request count."""
+    import bench
+    full, _ = bench.make_workload("c4", 300, 0)
+    full = full[0]
+    for world in (2, 3, 8):
+        parts = [bench.make_workload("c4", 300, r, world, "strong") for r in range(world)]
+        ids = [p[0][1] for p in parts]
+        sizes = [p[0][0].n_inst for p in parts]
+        assert ids == [sum(sizes[:r]) for r in range(world)] and sum(sizes) == full.n_inst
+        req = np.concatenate([p[0][0].req for p in parts])
+        assert np.array_equal(req, full.req)
+        assert parts[0][1]["shard_sizes"] == sizes
+        nreq = [p[0][0].n_req for p in parts]
+        assert max(nreq) - min(nreq) <= 2 * int(full.sizes().max())
