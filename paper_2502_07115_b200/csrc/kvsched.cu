@@ -18,6 +18,7 @@
 #include "kernel_lb.cuh"
 #include "kernel_prot.cuh"
 #include "kernel_ring.cuh"
+#include "kernel_mcring.cuh"
 #include "kernel_small.cuh"
 #include "kernel_lane.cuh"
 #include "kernel_flat.cuh"
@@ -51,6 +52,7 @@ struct sched_ctx {
     char err[512] = {0};
     const char *last_kernel = "";
     DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk, comp, fkeys;
+    DevBuf rq8, arr8, capv;                    // k_mc_prep -> k_mc_ring
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -77,7 +79,7 @@ struct sched_ctx {
     // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
     struct RunScratch {
         cudaStream_t stream = nullptr;
-        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp, fkeys;
+        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp, fkeys, rq8, arr8, capv;
     };
     RunScratch extra[7];
     std::vector<cudaEvent_t> chunk_events;
@@ -286,6 +288,9 @@ void swap_run_scratch(sched_ctx *c, sched_ctx::RunScratch &r)
     std::swap(c->retry, r.retry);
     std::swap(c->comp, r.comp);
     std::swap(c->fkeys, r.fkeys);
+    std::swap(c->rq8, r.rq8);
+    std::swap(c->arr8, r.arr8);
+    std::swap(c->capv, r.capv);
 }
 
 template <typename K>
@@ -699,7 +704,13 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     const int L_short = L_full < ring_short ? L_full : ring_short;
     P.L = L_short;
     const bool prot = pol->policy == SCHED_MCSF_PROTECTED;
-    auto wbytes = [&](int L) { return prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy); };
+    // MC policies with M <= 32767: the 16-bit profile ring with staged arrivals
+    // (kernel_mcring.cuh); KVSCHED_OLD_RING=1 keeps the 32-bit k_ring (A/B only)
+    const char *old_ring = getenv("KVSCHED_OLD_RING");
+    const bool mcr = mc && max_mem <= 32767 && !(old_ring && old_ring[0] == '1');
+    auto wbytes = [&](int L) {
+        return mcr ? mcring_warp_bytes(L, P.NP) : prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy);
+    };
     P.warp_bytes = wbytes(P.L);
     if ((size_t)P.warp_bytes > c->max_smem_optin)
         return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
@@ -731,7 +742,42 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     }
     const char *name = "";
     P.scratch_rows = (long long)slots;
-    if (pol->policy == SCHED_MCSF || prot) {
+    if (mcr) {
+        // k_mc_prep: statuses of invalid / unsupported instances, ranks, the rq8 / arr8
+        // streams and round caps; MC-SF instances with o~ > o get k_prot's entries instead
+        if ((rc = grow(c, c->rq8, slots * 8)) || (rc = grow(c, c->arr8, (slots + 64) * 8)) ||
+            (rc = grow(c, c->capv, ni * 4 + 4)))
+            return rc;
+        P.rq8 = reinterpret_cast<uint2 *>(c->rq8.p);
+        P.arr8 = reinterpret_cast<int2 *>(c->arr8.p);
+        P.capv = reinterpret_cast<int *>(c->capv.p);
+        if (early) {
+            if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
+            P.rq = reinterpret_cast<const uint4 *>(c->rq.p);
+            P.arank = reinterpret_cast<const int *>(c->arank.p);
+        }
+        const int ssmem = early ? next_pow2(max_req) * 4 : 16;
+        auto prep = early ? k_mc_prep<POL_MCSF> : k_mc_prep<POL_MCBENCH>;
+        CUDA_TRY(c, cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+        int per_sm = 1;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 1024, ssmem));
+        long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
+        if (blocks > inst->n_instances) blocks = inst->n_instances > 0 ? inst->n_instances : 1;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->timing) {
+            e0 = take_event(c);
+            e1 = take_event(c);
+            CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+        }
+        prep<<<(int)blocks, 1024, ssmem, c->stream>>>(P, reinterpret_cast<uint4 *>(c->rq.p),
+                                                       reinterpret_cast<int *>(c->arank.p));
+        CUDA_TRY(c, cudaGetLastError());
+        if (c->timing) {
+            CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+            c->pending.push_back({e0, e1, early ? "k_mc_prep<MCSF>" : "k_mc_prep<MCBENCH>"});
+        }
+        c->launches++;
+    } else if (pol->policy == SCHED_MCSF || prot) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
         // offsets are relative to the batch: scratch slot = request row (n_req <= slots)
         P.rq = reinterpret_cast<const uint4 *>(c->rq.p);
@@ -753,6 +799,14 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         P.relnext = reinterpret_cast<int *>(c->relnext.p);
     }
     auto launch_ring = [&](const KParams &Q) -> int {
+        if (mcr && pol->policy == SCHED_MCSF) {
+            name = "k_mc_ring<MCSF>";
+            return launch_sim(c, k_mc_ring<POL_MCSF>, Q, Q.warp_bytes, name);
+        }
+        if (mcr) {
+            name = "k_mc_ring<MCBENCH>";
+            return launch_sim(c, k_mc_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);
+        }
         switch (pol->policy) {
         case SCHED_MCSF: name = "k_ring<MCSF>"; return launch_sim(c, k_ring<POL_MCSF>, Q, Q.warp_bytes, name);
         case SCHED_MC_BENCH: name = "k_ring<MCBENCH>"; return launch_sim(c, k_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);

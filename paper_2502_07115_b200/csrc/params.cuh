@@ -46,6 +46,10 @@ struct KParams {
     // whose rows fall past it (only possible after an instance that broke the caller's
     // hint) is UNSUPPORTED instead of writing out of bounds
     long long scratch_rows;
+    // k_mc_prep -> k_mc_ring (kernel_mcring.cuh)
+    uint2 *rq8;                 // [rows] per rank: {s | w << 16, idx}
+    int2 *arr8;                 // [rows + 64] per idx (arrival order): {a, rank}
+    int *capv;                  // [n_inst] round cap, -1 = instance finished by k_mc_prep / k_prot
 };
 
 // Lane 0 writes the per-instance outputs.
