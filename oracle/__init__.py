@@ -24,7 +24,7 @@ _SRC = _HERE / "oracle.c"
 _LIB = _HERE / "liboracle.so"
 
 # policy ids of the oracle (its own numbering)
-MCSF, MCBENCH, ALPHA, ALPHA_BETA, MCSF_PROT = 0, 1, 2, 3, 4
+MCSF, MCBENCH, ALPHA, ALPHA_BETA, MCSF_PROT, MCSF_PROT_RAISE = 0, 1, 2, 3, 4, 5
 # instance status
 OK, INVALID, LIVELOCK = 0, 1, 2
 

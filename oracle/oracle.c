@@ -38,6 +38,9 @@
 #define OR_ALPHA 2       /* alpha-protection greedy           */
 #define OR_ALPHA_BETA 3  /* alpha-protection beta-clearing        */
 #define OR_MCSF_PROT 4   /* MC-SF on (1-alpha)M with clearing */
+#define OR_MCSF_PROT_RAISE 5  /* the same; a cleared request's o~ is raised to the
+                                 tokens it is known to need (DESIGN Q26b)          */
+#define OR_IS_PROT(p) ((p) == OR_MCSF_PROT || (p) == OR_MCSF_PROT_RAISE)
 
 /* at most this many beta passes per overflow (DESIGN Q29) */
 #define OR_BETA_MAX_PASSES 65536
@@ -131,7 +134,7 @@ typedef struct {
 /* R is kept as an array of request indices in the policy's key order. */
 static int or_key_less(const or_inst *I, int policy, int32_t x, int32_t y)
 {
-    if (policy == OR_MCSF || policy == OR_MCSF_PROT) {   /* (o~, idx): P:175, DESIGN Q5 */
+    if (policy == OR_MCSF || OR_IS_PROT(policy)) {       /* (o~, idx): P:175, DESIGN Q5 */
         if (I->op[x] != I->op[y]) return I->op[x] < I->op[y];
         return x < y;
     }
@@ -167,7 +170,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
 {
     for (int k = 0; k < 7; k++) stats[k] = 0;
     for (int64_t i = 0; i < n; i++) { completion[i] = -1; if (start) start[i] = -1; }
-    if (policy < OR_MCSF || policy > OR_MCSF_PROT) return -1;
+    if (policy < OR_MCSF || policy > OR_MCSF_PROT_RAISE) return -1;
     /* beta = beta_thresh / 2^32 must lie in (0, 1]: beta = 0 never clears (DESIGN Q29)    */
     if (policy == OR_ALPHA_BETA && (beta_thresh == 0 || beta_thresh > (1ull << 32))) return -1;
 
@@ -188,7 +191,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
     int64_t decision_rounds = 0, peak = 0, evictions = 0;
 
     /* ---- instance validation (DESIGN Q8) -------------------------------------------- */
-    if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || policy == OR_MCSF_PROT)
+    if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || OR_IS_PROT(policy))
         if (alpha_den <= 0 || alpha_num < 0 || alpha_num >= alpha_den) status = OR_INVALID;
     for (int64_t i = 0; i < n; i++) {
         if (s[i] < 1 || o[i] < 1 || op[i] < 1 || a[i] < 0) status = OR_INVALID;
@@ -216,12 +219,12 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
         }
         /* alpha budget B = floor((1 - alpha) M), alpha = num/den (DESIGN Q15) */
         int64_t B = 0;
-        if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || policy == OR_MCSF_PROT)
+        if (policy == OR_ALPHA || policy == OR_ALPHA_BETA || OR_IS_PROT(policy))
             B = ((int64_t)(alpha_den - alpha_num) * M) / alpha_den;
         /* Eq. 5's right-hand side: M, or (1-alpha)M for the protected MC-SF ("run MC-SF as
          * if the effective budget were (1-alpha)M")                               */
-        const int64_t budget = (policy == OR_MCSF_PROT) ? B : M;
-        const int use_pred = (policy == OR_MCSF || policy == OR_MCSF_PROT);
+        const int64_t budget = OR_IS_PROT(policy) ? B : M;
+        const int use_pred = (policy == OR_MCSF || OR_IS_PROT(policy));
 
         int64_t nR = 0, nS = 0, next = 0;
         int64_t t = a[0];
@@ -243,7 +246,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
             }
             if (nR > 0) decision_rounds++;
 
-            if (policy == OR_MCSF || policy == OR_MCBENCH || policy == OR_MCSF_PROT) {
+            if (policy == OR_MCSF || policy == OR_MCBENCH || OR_IS_PROT(policy)) {
                 /* Alg. 1 / Alg. 2: walk R in key order, add i
                  * to U while Eq. 5 holds for S and U+{i}; break at the first failure.    */
                 const int64_t idle_before = (nS == 0);
@@ -269,7 +272,7 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                 }
                 for (int64_t k = 0; k + nU < nR; k++) R[k] = R[k + nU];
                 nR -= nU;
-                if (policy == OR_MCSF_PROT) {
+                if (OR_IS_PROT(policy)) {
                     /* an underestimate o~ < o lets the realised KV growth pass M; "such an
                      * overflow triggers a clearing event, where all active requests are
                      * evicted and re-queued", with the cycle rule of DESIGN Q24   */
@@ -278,14 +281,20 @@ int or_simulate(int64_t n, const int32_t *req, int32_t M,
                     if (mem > M) {
                         for (int64_t k = 0; k < nS; k++) {
                             int32_t j = S[k];
+                            /* Q26b: j ran rounds p_j..t-1 and is not complete (c_j > t),
+                             * so o_j >= t - p_j + 1                                       */
+                            if (policy == OR_MCSF_PROT_RAISE && op[j] < t - p[j] + 1)
+                                op[j] = (int32_t)(t - p[j] + 1);
                             p[j] = -1; c[j] = -1;
                             or_insert_sorted(&I, policy, R, &nR, j);
                             evictions++;
                         }
                         nS = 0;
                         /* DESIGN Q24: only once every request has arrived is the run from
-                         * here a repeat of the last cycle (a later arrival may sort first) */
-                        if (next == n && have_clear && next == next_at_clear &&
+                         * here a repeat of the last cycle (a later arrival may sort first).
+                         * Not under Q26b: every clearing raises some o~ (the overflow needs
+                         * an active request past its predicted end), so no state repeats. */
+                        if (policy == OR_MCSF_PROT && next == n && have_clear && next == next_at_clear &&
                             completed_since_clear == 0) {
                             status = OR_LIVELOCK;
                             break;
@@ -465,7 +474,7 @@ int or_simulate_batch(int64_t n_inst, const int64_t *offset, const int32_t *req,
                       int64_t *decision_rounds, int32_t *makespan, int32_t *peak,
                       int64_t *evictions, int32_t *status)
 {
-    if (policy < OR_MCSF || policy > OR_MCSF_PROT) return -1;
+    if (policy < OR_MCSF || policy > OR_MCSF_PROT_RAISE) return -1;
     if (policy == OR_ALPHA_BETA && (beta_thresh == 0 || beta_thresh > (1ull << 32))) return -1;
     or_batch B = { n_inst, offset, req, mem, policy, alpha_num, alpha_den, beta_thresh, seed,
                    round_cap, gid0, completion, start, tel, rounds, decision_rounds, evictions,

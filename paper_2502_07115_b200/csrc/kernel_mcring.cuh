@@ -37,6 +37,7 @@
 
 namespace kv {
 
+#define KV_PREP_WARP_N 1024                  // k_mc_prep_w takes instances up to this size
 #define KV_STAGE_CH 32                       // arrival entries per staged chunk
 #define KV_STAGE_SLOTS 4                     // chunks resident / in flight per warp
 #define KV_STAGE_ENTRIES (KV_STAGE_CH + 2)   // one extra on each side for 16-byte alignment
@@ -152,54 +153,74 @@ __device__ __forceinline__ int2 stage_get(const Stage &S, int k)
 // ---------------------------------------------------------------------------------------
 struct R16 {
     uint16_t *p;
-    uint32_t *w;
-    int L, mask, hmask;
+    uint2 *q;           // quads: rounds 4j .. 4j+3 (mod L)
+    int L, mask, qmask;
 };
 
-// max over u in [1, w] of Prof(t+u) + u, split into u <= 31 (ma) and u >= 32 (mb); 0 if empty
-__device__ __forceinline__ void r16_window_max(const R16 &R, int t, int w, int &ma, int &mb)
+// in-window halfword masks of a quad: rounds t+u0 .. t+u0+3 against positions [1, e]
+__device__ __forceinline__ uint32_t half_in(int u, int e) { return (u >= 1 && u <= e) ? 0xffffu : 0u; }
+
+// The first-fit horizon: a blocked head is resolved for offsets D in [0, KV_FF_D]; position
+// u blocks D in [max(u-w, 0), min(u-1, Prof(t+u)+u-(M-s)-1, KV_FF_D)], so every position
+// u >= KV_FF_D + 1 inside the window (u <= w) blocks a prefix [0, ...] and only the maximum
+// of Prof(t+u)+u over them matters.  With four rounds per quad, the quads whose first
+// position is <= KV_FF_D + 1 ("head" quads, positions 1..A, A <= KV_FF_D + 4 = 31) are kept
+// apart from the rest, so the head positions are the only ones needing one lane each.
+#define KV_FF_D 27
+
+// max over u in [1, w] of Prof(t+u) + u: ma over the head quads (positions <= A), mb over
+// the rest; 0 if empty.  Four rounds per lane (one 8-byte shared load, two 16x2 adds, 128
+// rounds per warp pass); returns A, the last position of the head quads.
+__device__ __forceinline__ int r16_window_max(const R16 &R, int t, int w, int &ma, int &mb)
 {
     const int lane = lane_id();
     uint32_t acc_a = 0u, acc_b = 0u;
-    const int W0 = (t + 1) >> 1, W1 = (t + w) >> 1;
-    for (int jb = W0 + lane; jb <= W1; jb += 32) {
-        const uint32_t word = R.w[jb & R.hmask];
-        const int u0 = 2 * jb - t;                                   // 0 or 1 on the first word
-        const uint32_t z = __vadd2(word, (uint32_t)u0 | ((uint32_t)(u0 + 1) << 16));
-        const uint32_t in = (u0 >= 1 ? 0xffffu : 0u) | (u0 + 1 <= w ? 0xffff0000u : 0u);
-        const uint32_t lo31 = (u0 <= 31 ? 0xffffu : 0u) | (u0 + 1 <= 31 ? 0xffff0000u : 0u);
-        const uint32_t m = z & in;
-        acc_a = __vmaxu2(acc_a, m & lo31);
-        acc_b = __vmaxu2(acc_b, m & ~lo31);
+    const int Q0 = (t + 1) >> 2, Q1 = (t + w) >> 2;
+    // warp-uniform masks of the first quad (rounds <= t) and the last quad (rounds > t+w)
+    const unsigned long long fm = ~0ull << (16 * ((t + 1) & 3));
+    const unsigned long long em = ~0ull >> (16 * (3 - ((t + w) & 3)));
+    for (int q = Q0 + lane; q <= Q1; q += 32) {
+        const uint2 v = R.q[q & R.qmask];
+        const int u0 = 4 * q - t;                       // -2..1 on the first quad
+        uint32_t z0 = __vadd2(v.x, ((uint32_t)u0 & 0xffffu) | ((uint32_t)(u0 + 1) << 16));
+        uint32_t z1 = __vadd2(v.y, ((uint32_t)(u0 + 2) & 0xffffu) | ((uint32_t)(u0 + 3) << 16));
+        if (q == Q0) { z0 &= (uint32_t)fm; z1 &= (uint32_t)(fm >> 32); }
+        if (q == Q1) { z0 &= (uint32_t)em; z1 &= (uint32_t)(em >> 32); }
+        const uint32_t z = __vmaxu2(z0, z1);
+        if (u0 <= KV_FF_D + 1) acc_a = __vmaxu2(acc_a, z);
+        else acc_b = __vmaxu2(acc_b, z);
     }
     ma = (int)__reduce_max_sync(KV_FULL, max(acc_a & 0xffffu, acc_a >> 16));
     mb = (int)__reduce_max_sync(KV_FULL, max(acc_b & 0xffffu, acc_b >> 16));
+    const int qa = (t + KV_FF_D + 1) >> 2;              // quad holding position KV_FF_D + 1
+    return 4 * qa - t + 3;
 }
 
-// First offset D in [1, 31] at which (s, w) fits while the profile only advances, 32 if
-// none; the caller knows D = 0 fails.  mb = max_{32<=u<=w} Prof(t+u) + u.  Needs w+31 <= L.
-__device__ __forceinline__ int r16_first_fit(const R16 &R, int t, int w, int room, int mb)
+// First offset D in [1, KV_FF_D] at which (s, w) fits while the profile only advances,
+// KV_FF_D + 1 if none; the caller knows D = 0 fails.  mb = max Prof(t+u)+u over the window
+// positions A+1..w (A from r16_window_max, KV_FF_D + 1 <= A <= KV_FF_D + 4).  Needs
+// w + KV_FF_D <= L.
+__device__ __forceinline__ int r16_first_fit(const R16 &R, int t, int w, int room, int A, int mb)
 {
     const int lane = lane_id();
     uint32_t cov = 0u;
-    const int gb = mb - room - 1;                          // positions 32..w block [0, gb]
-    if (gb >= 0) cov = gb >= 31 ? KV_FULL : (0xffffffffu >> (31 - gb));
-    if (lane < 31) {
-        const int ua = lane + 1;                           // positions 1..31
-        if (ua <= w + 31) {
-            const int v = R.p[(t + ua) & R.mask];
-            const int lo = max(ua - w, 0), hi = min(ua - 1, v + ua - room - 1);
-            if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
-        }
-        const int uc = max(32, w + 1) + lane;              // positions max(32, w+1)..w+31
-        if (uc <= w + 31) {
-            const int v = R.p[(t + uc) & R.mask];
-            const int lo = uc - w, hi = min(31, v + uc - room - 1);
-            if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
-        }
+    const uint32_t all = 0xffffffffu >> (31 - KV_FF_D);
+    const int gb = mb - room - 1;                          // positions A+1..w block [0, gb]
+    if (gb >= 0) cov = gb >= KV_FF_D ? all : (0xffffffffu >> (31 - gb));
+    if (lane < A) {
+        const int ua = lane + 1;                           // head positions 1..A
+        const int v = R.p[(t + ua) & R.mask];
+        const int lo = max(ua - w, 0), hi = min(min(ua - 1, v + ua - room - 1), KV_FF_D);
+        if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
+    }
+    const int uc = max(A, w) + 1 + lane;                   // positions max(A, w)+1 .. w+KV_FF_D
+    if (uc <= w + KV_FF_D) {
+        const int v = R.p[(t + uc) & R.mask];
+        const int lo = uc - w, hi = min(v + uc - room - 1, KV_FF_D);
+        if (hi >= lo) cov |= (0xffffffffu >> (31 - hi)) & (0xffffffffu << lo);
     }
     cov = __reduce_or_sync(KV_FULL, cov);
-    return cov == KV_FULL ? 32 : __ffs(~cov) - 1;
+    return cov == all ? KV_FF_D + 1 : __ffs(~cov) - 1;
 }
 
 __device__ __forceinline__ int r16_at(const R16 &R, const LongList &G, int t, int u)
@@ -230,16 +251,25 @@ __device__ __forceinline__ int r16_fit_slow(const R16 &R, const LongList &G, int
     return cov == KV_FULL ? 32 : __ffs(~cov) - 1;
 }
 
-// Prof(t+u) += s + u for u in [1, min(w, L)] (two rounds per lane and word)
+// Prof(t+u) += s + u for u in [1, min(w, L)] (four rounds per lane: one 8-byte load/store;
+// a halfword never carries: the sum is <= M, certified by the Eq. 5 test)
 __device__ __forceinline__ void r16_ramp(const R16 &R, int t, int w, int s)
 {
     const int e = min(w, R.L);
-    const int W0 = (t + 1) >> 1, W1 = (t + e) >> 1;
-    for (int jb = W0 + lane_id(); jb <= W1; jb += 32) {
-        const int u0 = 2 * jb - t;
-        const uint32_t lo = u0 >= 1 ? (uint32_t)(s + u0) : 0u;
-        const uint32_t hi = u0 + 1 <= e ? (uint32_t)(s + u0 + 1) : 0u;
-        R.w[jb & R.hmask] += lo | (hi << 16);
+    const int Q0 = (t + 1) >> 2, Q1 = (t + e) >> 2;
+    const unsigned long long fm = ~0ull << (16 * ((t + 1) & 3));
+    const unsigned long long em = ~0ull >> (16 * (3 - ((t + e) & 3)));
+    for (int q = Q0 + lane_id(); q <= Q1; q += 32) {
+        const int u0 = 4 * q - t;
+        const int b = s + u0;
+        uint32_t a0 = ((uint32_t)b & 0xffffu) | ((uint32_t)(b + 1) << 16);
+        uint32_t a1 = ((uint32_t)(b + 2) & 0xffffu) | ((uint32_t)(b + 3) << 16);
+        if (q == Q0) { a0 &= (uint32_t)fm; a1 &= (uint32_t)(fm >> 32); }
+        if (q == Q1) { a0 &= (uint32_t)em; a1 &= (uint32_t)(em >> 32); }
+        uint2 v = R.q[q & R.qmask];
+        v.x += a0;
+        v.y += a1;
+        R.q[q & R.qmask] = v;
     }
 }
 
@@ -248,6 +278,14 @@ __device__ __forceinline__ void r16_ramp(const R16 &R, int t, int w, int s)
 __device__ __forceinline__ int r16_jump(const R16 &R, LongList &G, int t, int E, int tn)
 {
     const int lane = lane_id();
+    if (tn == t + 1 && E == tn && !G.used) {            // the common single-round advance
+        const int slot = tn & R.mask;
+        const int v = R.p[slot];
+        __syncwarp();
+        if (lane == 0) R.p[slot] = 0;
+        __syncwarp();
+        return v;
+    }
     const int L = R.L, mask = R.mask;
     int v = 0;
     const int dn = max(min(E - t, L), 0);
@@ -274,7 +312,7 @@ __device__ __forceinline__ int r16_jump(const R16 &R, LongList &G, int t, int E,
             R.p[j] = (uint16_t)far;
         }
     }
-    G.used &= ~__ballot_sync(KV_FULL, ((G.used >> lane) & 1u) && G.e <= tn + L);
+    if (G.used) G.used &= ~__ballot_sync(KV_FULL, ((G.used >> lane) & 1u) && G.e <= tn + L);
     __syncwarp();
     return warp_max_i32(v);
 }
@@ -283,6 +321,14 @@ __host__ __device__ inline int mcring_warp_bytes(int L, int NP)
 {
     const int b = KV_STAGE_SLOTS * 8 + KV_STAGE_SLOTS * KV_STAGE_ENTRIES * 8 + L * 2 + (NP / 32) * 4 + 32 * 4;
     return (b + 15) & ~15;
+}
+
+// Work estimate of an instance for longest-first claiming (rounds ~ the larger of the
+// arrival span and the volume the budget must carry; plus one admission per request)
+__device__ __forceinline__ uint32_t work_estimate(int a0, int alast, long long vol, int M, int n)
+{
+    const long long r = max((long long)alast - a0, vol / max(M, 1)) + n;
+    return (uint32_t)min(r + 1, 0xffffffffll);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -294,20 +340,22 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem_raw);
     __shared__ int s_flags;                 // bit 0 invalid, bit 1 unsupported, bit 2 o~ != o
-    __shared__ unsigned long long s_sumo;
+    __shared__ unsigned long long s_sumo, s_vol;
     const int tid = threadIdx.x, lane = tid & 31;
     const int *reqi = reinterpret_cast<const int *>(P.req);
     for (long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
+        if (n <= KV_PREP_WARP_N) continue;                // k_mc_prep_w
         const int M = P.mem[inst];
         if (tid == 0) {
             s_flags = (n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows) ? 2 : 0;
             s_sumo = 0ull;
+            s_vol = 0ull;
         }
         __syncthreads();
         int fl = 0;
-        long long so = 0;
+        long long so = 0, vol = 0;
         if (!(s_flags & 2)) {
             for (int k = tid; k < n; k += blockDim.x) {
                 const int4 r = P.req[off + k];
@@ -322,14 +370,17 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
                 if (r.z > P.max_len || (POL == POL_MCSF && r.w > P.max_len)) fl |= 2;
                 if (bad) fl |= 1;
                 so += r.z;
+                vol += (long long)r.y * r.z + (long long)r.z * (r.z + 1) / 2;
                 if (POL == POL_MCSF) keys[k] = ((uint32_t)min(max(r.w, 0), 0x1ffff) << 15) | (uint32_t)k;
             }
         }
         fl = __reduce_or_sync(KV_FULL, fl);
         so = warp_sum_i64(so);
+        vol = warp_sum_i64(vol);
         if (lane == 0) {
             if (fl) atomicOr(&s_flags, fl);
             if (so) atomicAdd(&s_sumo, (unsigned long long)so);
+            if (vol) atomicAdd(&s_vol, (unsigned long long)vol);
         }
         __syncthreads();
         const int flags = s_flags;
@@ -389,8 +440,118 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
                 capv = (int)min(cap64, 0x7ffffffell);
             }
         }
-        if (tid == 0) P.capv[inst] = capv;
+        if (tid == 0) {
+            P.capv[inst] = capv;
+            if (P.estv) P.estv[inst] = capv < 0 ? 0u : work_estimate(reqi[off * 4], reqi[(off + n - 1) * 4],
+                                                                     (long long)s_vol, M, n);
+        }
         __syncthreads();
+    }
+}
+
+// k_mc_prep_w: the same for instances of at most KV_PREP_WARP_N requests, one warp each
+// (keys in 4 KB of shared memory per warp, the bitonic stages separated by __syncwarp
+// instead of block barriers); k_mc_prep then takes only the larger instances.
+template <int POL>
+__global__ void __launch_bounds__(256) k_mc_prep_w(const KParams P, uint4 *rq_early, int *arank_early)
+{
+    __shared__ __align__(16) uint32_t keys_all[8][KV_PREP_WARP_N];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *keys = keys_all[warp];
+    const int *reqi = reinterpret_cast<const int *>(P.req);
+    const long long nwarps = (long long)gridDim.x * 8;
+    for (long long inst = (long long)blockIdx.x * 8 + warp; inst < P.n_inst; inst += nwarps) {
+        const long long off = P.offset[inst] - P.row_base;
+        const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
+        if (n > KV_PREP_WARP_N) continue;                  // k_mc_prep
+        const int M = P.mem[inst];
+        int fl = (n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows) ? 2 : 0;
+        long long so = 0, vol = 0;
+        if (!fl) {
+            int carry = 0;                                 // a of row k0 - 1
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const int4 r = k < n ? P.req[off + k] : make_int4(0x7fffffff, 1, 1, 1);
+                int prev = __shfl_up_sync(KV_FULL, r.x, 1);
+                if (lane == 0) prev = carry;
+                carry = __shfl_sync(KV_FULL, r.x, 31);
+                if (k < n) {
+                    bool bad = r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1 || (k > 0 && prev > r.x);
+                    if (POL == POL_MCSF) {
+                        bad |= (long long)r.y + r.w > M || r.w < r.z;
+                        if (r.w != r.z) fl |= 4;
+                    } else {
+                        bad |= (long long)r.y + r.z > M;
+                    }
+                    if (r.z > P.max_len || (POL == POL_MCSF && r.w > P.max_len)) fl |= 2;
+                    if (bad) fl |= 1;
+                    so += r.z;
+                    vol += (long long)r.y * r.z + (long long)r.z * (r.z + 1) / 2;
+                    if (POL == POL_MCSF) keys[k] = ((uint32_t)min(max(r.w, 0), 0x1ffff) << 15) | (uint32_t)k;
+                }
+            }
+        }
+        fl = __reduce_or_sync(KV_FULL, fl);
+        so = warp_sum_i64(so);
+        vol = warp_sum_i64(vol);
+        int capv = -1;
+        if (fl & 3) {
+            for (int k = lane; k < n; k += 32) {
+                if (P.completion) P.completion[off + k] = -1;
+                if (P.start) P.start[off + k] = -1;
+            }
+            write_result(P, inst, InstResult{0, 0, 0, 0, 0, 0, (fl & 2) ? ST_UNSUPPORTED : ST_INVALID});
+        } else if (n == 0) {
+            write_result(P, inst, InstResult{0, 0, 0, 0, 0, 0, ST_OK});
+        } else if (POL == POL_MCSF && (fl & 4) && !P.early_list) {
+            for (int k = lane; k < n; k += 32) {
+                if (P.completion) P.completion[off + k] = -1;
+                if (P.start) P.start[off + k] = -1;
+            }
+            write_result(P, inst, InstResult{0, 0, 0, 0, 0, 0, ST_UNSUPPORTED});
+        } else {
+            if (POL == POL_MCSF) {
+                const int NPi = next_pow2(max(n, 2));
+                for (int k = n + lane; k < NPi; k += 32) keys[k] = 0xffffffffu;
+                __syncwarp();
+                for (int k = 2; k <= NPi; k <<= 1) {
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        for (int i = lane; i < (NPi >> 1); i += 32) {
+                            const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+                            const int hi = lo + j;
+                            const bool up = (lo & k) == 0;
+                            const uint32_t x = keys[lo], y = keys[hi];
+                            if ((x > y) == up) { keys[lo] = y; keys[hi] = x; }
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            if (POL == POL_MCSF && (fl & 4)) {
+                for (int r = lane; r < n; r += 32) {
+                    const int idx = (int)(keys[r] & 0x7fffu);
+                    const int4 q = P.req[off + idx];
+                    rq_early[off + r] = make_uint4((uint32_t)q.y, (uint32_t)q.w, (uint32_t)q.z, (uint32_t)idx);
+                    arank_early[off + idx] = r;
+                }
+                if (lane == 0) P.early_list[atomicAdd(P.early_count, 1ull)] = inst;
+            } else {
+                for (int r = lane; r < n; r += 32) {
+                    const int idx = POL == POL_MCSF ? (int)(keys[r] & 0x7fffu) : r;
+                    const int4 q = P.req[off + idx];
+                    const int w = POL == POL_MCSF ? q.w : q.z;
+                    P.rq8[off + r] = make_uint2((uint32_t)q.y | ((uint32_t)w << 16), (uint32_t)idx);
+                    P.arr8[off + idx] = make_int2(q.x, r);
+                }
+                const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], so);
+                capv = (int)min(cap64, 0x7ffffffell);
+            }
+        }
+        if (lane == 0) {
+            P.capv[inst] = capv;
+            if (P.estv) P.estv[inst] = capv < 0 ? 0u : work_estimate(reqi[off * 4], reqi[(off + n - 1) * 4], vol, M, n);
+        }
+        __syncwarp();
     }
 }
 
@@ -412,7 +573,7 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
 
     const int NPi = next_pow2(max(n, 32));
     const int nw = NPi >> 5;
-    for (int i = lane; i < (L >> 1); i += 32) R.w[i] = 0u;
+    for (int i = lane; i < (L >> 2); i += 32) R.q[i] = make_uint2(0u, 0u);
     for (int w = lane; w < nw; w += 32) bm[w] = 0u;
     smq[lane] = 0u;
     __syncwarp();
@@ -483,15 +644,20 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
             const int s = (int)(he.x & 0xffffu), w = (int)(he.x >> 16), idx = (int)he.y;
             if (!head_fits) {
                 int d;
-                if (w + 31 <= L) {
+                if (w + KV_FF_D + 4 <= L) {
                     int ma, mb;
-                    r16_window_max(R, t, w, ma, mb);
+                    const int A = r16_window_max(R, t, w, ma, mb);
                     const int room = M - s;
-                    d = max(ma, mb) <= room ? 0 : (multi ? r16_first_fit(R, t, w, room, mb) : 1);
+                    d = max(ma, mb) <= room ? 0 : (multi ? r16_first_fit(R, t, w, room, A, mb) : 1);
+                    if (d == KV_FF_D + 1) d = 32;          // blocked throughout: jump KV_FF_D + 1
                 } else {
                     d = r16_fit_slow(R, G, t, s, w, M, multi);
                 }
-                if (d > 0) { jump = d; blocked_through = d == 32; break; }   // Eq. 5 violated
+                if (d > 0) {                               // Eq. 5 violated
+                    blocked_through = d == 32;
+                    jump = blocked_through ? (w + KV_FF_D + 4 <= L ? KV_FF_D + 1 : 32) : d;
+                    break;
+                }
             }
             head_fits = false;
             // MC-SF: the next head leaves the queue first so that its entry loads while the
@@ -574,8 +740,11 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
     write_result(P, inst, res);
 }
 
+#ifndef KV_MCRING_MINB
+#define KV_MCRING_MINB 8        // blocks of 4 warps per SM the register budget must allow
+#endif
 template <int POL>
-__global__ void __launch_bounds__(128) k_mc_ring(const KParams P)
+__global__ void __launch_bounds__(128, KV_MCRING_MINB) k_mc_ring(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -586,10 +755,10 @@ __global__ void __launch_bounds__(128) k_mc_ring(const KParams P)
     unsigned char *rp = base + KV_STAGE_SLOTS * 8 + KV_STAGE_SLOTS * KV_STAGE_ENTRIES * 8;
     R16 R;
     R.p = reinterpret_cast<uint16_t *>(rp);
-    R.w = reinterpret_cast<uint32_t *>(rp);
+    R.q = reinterpret_cast<uint2 *>(rp);
     R.L = P.L;
     R.mask = P.L - 1;
-    R.hmask = (P.L >> 1) - 1;
+    R.qmask = (P.L >> 2) - 1;
     uint32_t *bm = reinterpret_cast<uint32_t *>(rp + P.L * 2);
     uint32_t *smq = bm + P.NP / 32;
     if (lane == 0)

@@ -4,6 +4,7 @@
 // launch on the context's stream.  All simulation work runs in the kernels of
 // kernel_small.cuh / kernel_ring.cuh; there is no CPU path.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -52,7 +53,7 @@ struct sched_ctx {
     char err[512] = {0};
     const char *last_kernel = "";
     DevBuf counter, bounds, rq, arank, pstart, relnext, total, retry, scan, dec, h_pk, comp, fkeys;
-    DevBuf rq8, arr8, capv;                    // k_mc_prep -> k_mc_ring
+    DevBuf rq8, arr8, capv, lpt;               // k_mc_prep -> k_mc_ring
     DevBuf h_off, h_req, h_mem, h_out;         // device staging for the host path
     // accounting
     long long launches = 0, sim_launches = 0;
@@ -79,7 +80,7 @@ struct sched_ctx {
     // kernels of consecutive chunks overlap (one chunk's tail with the next one's start)
     struct RunScratch {
         cudaStream_t stream = nullptr;
-        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp, fkeys, rq8, arr8, capv;
+        DevBuf counter, bounds, rq, arank, pstart, relnext, retry, comp, fkeys, rq8, arr8, capv, lpt;
     };
     RunScratch extra[7];
     std::vector<cudaEvent_t> chunk_events;
@@ -291,6 +292,7 @@ void swap_run_scratch(sched_ctx *c, sched_ctx::RunScratch &r)
     std::swap(c->rq8, r.rq8);
     std::swap(c->arr8, r.arr8);
     std::swap(c->capv, r.capv);
+    std::swap(c->lpt, r.lpt);
 }
 
 template <typename K>
@@ -313,8 +315,16 @@ int warps_per_block(const sched_ctx *c, int warp_bytes)
     return w;
 }
 
+// ids[i] = i, *count = n (the value list and count of the longest-first work list)
+__global__ void k_iota(long long n, long long *ids, unsigned long long *count)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        ids[i] = i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)n;
+}
+
 template <typename K>
-int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const char *name)
+int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const char *name, int max_warps_per_sm = 0)
 {
     const int wpb = warps_per_block(c, warp_bytes);
     const int block = 32 * wpb, smem = warp_bytes * wpb;
@@ -324,6 +334,20 @@ int launch_sim(sched_ctx *c, K kernel, const KParams &P, int warp_bytes, const c
     int grid = 1;
     int rc = occupancy_grid(c, kernel, block, smem, P.n_inst, &grid);
     if (rc) return rc;
+    if (max_warps_per_sm < 0) {
+        // longest-first claiming with fewer instances than two full waves (C3: 4096 long
+        // instances): 16 resident warps per SM, so the longest instances, which start first,
+        // run with fewer warps beside them (measured on C3: 29.4 ms vs 34-36 ms at full
+        // occupancy, 35 ms at 12, 44 ms at 8; C4, 4x the resident warps, is best full)
+        int per_sm = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
+        const long long full = (long long)per_sm * wpb * c->num_sms;
+        max_warps_per_sm = P.n_inst < 2 * full ? 16 : 0;
+    }
+    if (max_warps_per_sm > 0) {           // fewer resident warps
+        const long long cap = (long long)((max_warps_per_sm + wpb - 1) / wpb) * c->num_sms;
+        if (grid > cap) grid = (int)cap;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
         e0 = take_event(c);
@@ -742,6 +766,15 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     }
     const char *name = "";
     P.scratch_rows = (long long)slots;
+    bool lpt = false;
+    uint32_t *lpt_est = nullptr, *lpt_est_sorted = nullptr;
+    long long *lpt_ids = nullptr, *lpt_order = nullptr;
+    unsigned long long *lpt_count = nullptr;
+    void *lpt_tmp = nullptr;
+    size_t lpt_tmp_bytes = 0;
+    // resident warps per SM of the longest-first launch (KVSCHED_MCRING_WPS: experiments)
+    int mcring_wps = -1;                // -1: the rule in launch_sim
+    if (const char *e = getenv("KVSCHED_MCRING_WPS")) mcring_wps = atoi(e);
     if (mcr) {
         // k_mc_prep: statuses of invalid / unsupported instances, ranks, the rq8 / arr8
         // streams and round caps; MC-SF instances with o~ > o get k_prot's entries instead
@@ -751,32 +784,77 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         P.rq8 = reinterpret_cast<uint2 *>(c->rq8.p);
         P.arr8 = reinterpret_cast<int2 *>(c->arr8.p);
         P.capv = reinterpret_cast<int *>(c->capv.p);
+        // longest-first claiming (KVSCHED_LPT=0 turns it off, A/B only): the prep writes a
+        // work estimate per instance, a radix sort orders the ids by it, and the simulation
+        // claims from that list; layout est | est_sorted | ids | order | count | cub temp
+        const char *lpt_env = getenv("KVSCHED_LPT");
+        lpt = ni > 1 && ni < (1ull << 31) && !(lpt_env && lpt_env[0] == '0');
+        if (lpt) {
+            size_t tmp = 0;
+            cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                      (const long long *)nullptr, (long long *)nullptr, (int)ni, 0, 32,
+                                                      c->stream);
+            const size_t a8 = (ni * 4 + 15) & ~(size_t)15;
+            if ((rc = grow(c, c->lpt, 2 * a8 + 2 * ni * 8 + 16 + tmp + 256))) return rc;
+            char *b = reinterpret_cast<char *>(c->lpt.p);
+            lpt_est = reinterpret_cast<uint32_t *>(b);
+            lpt_est_sorted = reinterpret_cast<uint32_t *>(b + a8);
+            lpt_ids = reinterpret_cast<long long *>(b + 2 * a8);
+            lpt_order = lpt_ids + ni;
+            lpt_count = reinterpret_cast<unsigned long long *>(lpt_order + ni);
+            lpt_tmp = b + 2 * a8 + 2 * ni * 8 + 16;
+            lpt_tmp_bytes = tmp;
+            P.estv = lpt_est;
+            k_iota<<<(int)std::min<long long>((long long)(ni + 255) / 256, 4LL * c->num_sms), 256, 0, c->stream>>>(
+                (long long)ni, lpt_ids, lpt_count);
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        }
         if (early) {
             if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
             P.rq = reinterpret_cast<const uint4 *>(c->rq.p);
             P.arank = reinterpret_cast<const int *>(c->arank.p);
         }
-        const int ssmem = early ? next_pow2(max_req) * 4 : 16;
-        auto prep = early ? k_mc_prep<POL_MCSF> : k_mc_prep<POL_MCBENCH>;
-        CUDA_TRY(c, cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
-        int per_sm = 1;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 1024, ssmem));
-        long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
-        if (blocks > inst->n_instances) blocks = inst->n_instances > 0 ? inst->n_instances : 1;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (c->timing) {
             e0 = take_event(c);
             e1 = take_event(c);
             CUDA_TRY(c, cudaEventRecord(e0, c->stream));
         }
-        prep<<<(int)blocks, 1024, ssmem, c->stream>>>(P, reinterpret_cast<uint4 *>(c->rq.p),
-                                                       reinterpret_cast<int *>(c->arank.p));
-        CUDA_TRY(c, cudaGetLastError());
+        uint4 *rq_e = reinterpret_cast<uint4 *>(c->rq.p);
+        int *ar_e = reinterpret_cast<int *>(c->arank.p);
+        {   // instances of <= KV_PREP_WARP_N requests: one warp each
+            auto prep_w = early ? k_mc_prep_w<POL_MCSF> : k_mc_prep_w<POL_MCBENCH>;
+            int per_sm = 1;
+            CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_w, 256, 0));
+            long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
+            const long long need = (inst->n_instances + 7) / 8;
+            if (blocks > need) blocks = need > 0 ? need : 1;
+            prep_w<<<(int)blocks, 256, 0, c->stream>>>(P, rq_e, ar_e);
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        }
+        if (max_req > KV_PREP_WARP_N) {   // larger instances: one CTA each
+            const int ssmem = early ? next_pow2(max_req) * 4 : 16;
+            auto prep = early ? k_mc_prep<POL_MCSF> : k_mc_prep<POL_MCBENCH>;
+            CUDA_TRY(c, cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+            int per_sm = 1;
+            CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 1024, ssmem));
+            long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
+            if (blocks > inst->n_instances) blocks = inst->n_instances > 0 ? inst->n_instances : 1;
+            prep<<<(int)blocks, 1024, ssmem, c->stream>>>(P, rq_e, ar_e);
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        }
+        if (lpt) {
+            CUDA_TRY(c, cub::DeviceRadixSort::SortPairsDescending(lpt_tmp, lpt_tmp_bytes, lpt_est, lpt_est_sorted,
+                                                                  lpt_ids, lpt_order, (int)ni, 0, 32, c->stream));
+            c->launches++;
+        }
         if (c->timing) {
             CUDA_TRY(c, cudaEventRecord(e1, c->stream));
             c->pending.push_back({e0, e1, early ? "k_mc_prep<MCSF>" : "k_mc_prep<MCBENCH>"});
         }
-        c->launches++;
     } else if (pol->policy == SCHED_MCSF || prot) {
         if ((rc = grow(c, c->rq, slots * 16)) || (rc = grow(c, c->arank, slots * 4))) return rc;
         // offsets are relative to the batch: scratch slot = request row (n_req <= slots)
@@ -798,15 +876,20 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         if ((rc = grow(c, c->relnext, slots * 4))) return rc;
         P.relnext = reinterpret_cast<int *>(c->relnext.p);
     }
-    auto launch_ring = [&](const KParams &Q) -> int {
-        if (mcr && pol->policy == SCHED_MCSF) {
-            name = "k_mc_ring<MCSF>";
-            return launch_sim(c, k_mc_ring<POL_MCSF>, Q, Q.warp_bytes, name);
-        }
+    auto launch_ring = [&](const KParams &Q0) -> int {
         if (mcr) {
-            name = "k_mc_ring<MCBENCH>";
-            return launch_sim(c, k_mc_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);
+            KParams Q = Q0;
+            int wps = 0;
+            if (lpt && !Q.work_list) {         // first launch: claim longest first
+                Q.work_list = lpt_order;
+                Q.work_count = lpt_count;
+                wps = mcring_wps;
+            }
+            name = pol->policy == SCHED_MCSF ? "k_mc_ring<MCSF>" : "k_mc_ring<MCBENCH>";
+            return pol->policy == SCHED_MCSF ? launch_sim(c, k_mc_ring<POL_MCSF>, Q, Q.warp_bytes, name, wps)
+                                             : launch_sim(c, k_mc_ring<POL_MCBENCH>, Q, Q.warp_bytes, name, wps);
         }
+        const KParams &Q = Q0;
         switch (pol->policy) {
         case SCHED_MCSF: name = "k_ring<MCSF>"; return launch_sim(c, k_ring<POL_MCSF>, Q, Q.warp_bytes, name);
         case SCHED_MC_BENCH: name = "k_ring<MCBENCH>"; return launch_sim(c, k_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);

@@ -50,6 +50,7 @@ struct KParams {
     uint2 *rq8;                 // [rows] per rank: {s | w << 16, idx}
     int2 *arr8;                 // [rows + 64] per idx (arrival order): {a, rank}
     int *capv;                  // [n_inst] round cap, -1 = instance finished by k_mc_prep / k_prot
+    uint32_t *estv;             // [n_inst] work estimate (0 = nothing to simulate) or null
 };
 
 // Lane 0 writes the per-instance outputs.

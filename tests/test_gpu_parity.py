@@ -263,7 +263,7 @@ def test_prediction_overestimate_ring(K, ctx, oracle_mod, shape, flags):
     finally:
         ctx.set_timing(False)
         ctx.reset_stats()
-    assert "k_prot<MCSF,early>" in names and "k_ring<MCSF>" in names, names
+    assert "k_prot<MCSF,early>" in names and ("k_mc_ring<MCSF>" in names or "k_ring<MCSF>" in names), names
     assert (o["status"] == 0).sum() > 0
 
 
@@ -847,3 +847,23 @@ def test_lane_scope_far_arrivals(K, ctx, oracle_mod):
     b = W.from_instances(insts)
     for pol in (0, 1):
         check(K, ctx, oracle_mod, b, pol, "far arrivals")
+
+
+# ---------------------------------------------------------------------------------------
+# Round 2: every-output parity at the configured sizes of C3 and C4 (BASELINE configs[2],
+# configs[3])
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("lam", [0.4, 2.0])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_c3_every_instance(K, ctx, oracle_mod, lam, pol):
+    """C3 (trace-shaped, 10^4 requests per instance, M = 16492): 256 instances per lambda and
+    MC policy, every output of every instance against the oracle."""
+    b = W.c3(256, 300 + int(10 * lam), lam)
+    check(K, ctx, oracle_mod, b, pol, f"C3 256 lam={lam}")
+
+
+def test_c4_full_config_mcsf(K, ctx, oracle_mod):
+    """C4 at the configured 10^5 instances (Table-1 regime, 1000 requests each), MC-SF, one
+    launch, every output of every instance against the oracle."""
+    b = W.c4(100_000, 4)
+    check(K, ctx, oracle_mod, b, 0, "C4 10^5 MC-SF")
