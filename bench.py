@@ -501,42 +501,52 @@ def main():
                   warp_value=rounds_rank * world / (wp_ms / 1000.0),
                   speedup_over_warp=wp_ms / (ms_max / args.steps))
 
-    # configs[1] (C2, AM1: 10^4 instances of 1000 requests at t=0, M=40) under the same
-    # protocol, reported beside the primary workload
+    # The other BASELINE configs under the same protocol (inputs resident, CUDA events on the
+    # launching stream, max over ranks), reported beside the primary workload: configs[1]
+    # (C2: AM1, 10^4 instances of 1000 requests at t=0, M=40), configs[3] (C4: trace-shaped,
+    # 2*10^4 instances of 1000 requests, M=16492) and configs[2] (C3: trace-shaped, 4096
+    # instances of 10^4 requests); MC-SF.
     also = None
     if not args.no_also and args.workload == "c5" and args.policy == "mcsf":
-        (b2, id2), cfg2 = make_workload("c2", 0, rank, world, args.split)
-        o2, r2, m2 = K.to_device(b2, dev)
-        out2 = K.alloc_outputs(b2.n_inst, b2.n_req, dev, fields)
-        h2 = K.hints_of(b2)
-        for _ in range(max(args.warmup, 1)):
-            ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
-        torch.cuda.synchronize(dev)
-        rounds2 = int(out2["rounds"][:b2.n_inst].clamp(min=0).sum().item())
-        if world > 1:
-            dist.barrier()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ctx.reset_stats()
-        ctx.set_timing(True)
-        h0.record(stream)
-        for _ in range(args.steps):
-            ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
-        h1.record(stream)
-        torch.cuda.synchronize(dev)
-        t2 = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
-        n2 = torch.tensor([rounds2], dtype=torch.int64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-            dist.all_reduce(n2)
-        ms2 = float(t2.item())
-        ctx.set_timing(False)
-        kst2 = ctx.kernel_stats()
-        also = {"C2": {"workload": cfg2["workload"], "instances_per_gpu": b2.n_inst,
-                       "value": int(n2.item()) * args.steps / (ms2 / 1e3), "unit": UNIT,
-                       "ms_per_step": ms2 / args.steps,
-                       "kernel": max(kst2, key=lambda k: kst2[k][0]) if kst2 else ctx.last_kernel(),
-                       "kernels_ms_per_step": {k: v[0] / args.steps for k, v in kst2.items()}}}
-        del o2, r2, m2, out2
+        also = {}
+        for wl, label in (("c2", "C2"), ("c4", "C4"), ("c3", "C3")):
+            (b2, id2), cfg2 = make_workload(wl, 0, rank, world, args.split)
+            cfg2.pop("shard_sizes", None)
+            o2, r2, m2 = K.to_device(b2, dev)
+            out2 = K.alloc_outputs(b2.n_inst, b2.n_req, dev, fields)
+            h2 = K.hints_of(b2)
+            for _ in range(max(args.warmup, 1)):
+                ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
+            torch.cuda.synchronize(dev)
+            rounds2 = int(out2["rounds"][:b2.n_inst].clamp(min=0).sum().item())
+            ok2 = int((out2["status"][:b2.n_inst] == 0).sum().item())
+            if world > 1:
+                dist.barrier()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ctx.reset_stats()
+            ctx.set_timing(True)
+            steps2 = args.steps if wl != "c3" else max(1, min(args.steps, 5))
+            h0.record(stream)
+            for _ in range(steps2):
+                ctx.run(o2, r2, m2, pol, out2, id0=id2, hints=h2)
+            h1.record(stream)
+            torch.cuda.synchronize(dev)
+            t2 = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+            n2 = torch.tensor([rounds2, ok2, b2.n_inst], dtype=torch.int64, device=dev)
+            if world > 1:
+                dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+                dist.all_reduce(n2)
+            ms2 = float(t2.item())
+            ctx.set_timing(False)
+            kst2 = ctx.kernel_stats()
+            r_all, ok_all2, ni_all = (int(x) for x in n2.tolist())
+            also[label] = {"workload": cfg2["workload"], "instances": ni_all, "instances_ok": ok_all2,
+                           "value": r_all * steps2 / (ms2 / 1e3), "unit": UNIT, "steps": steps2,
+                           "ms_per_step": ms2 / steps2, "rounds_per_step": r_all,
+                           "kernel": max(kst2, key=lambda k: kst2[k][0]) if kst2 else ctx.last_kernel(),
+                           "kernels_ms_per_step": {k: v[0] / steps2 for k, v in kst2.items()}}
+            del o2, r2, m2, out2, b2
+            torch.cuda.empty_cache()
 
     # rank 0: the gathered per-instance rows of the last timed step, in global instance order
     if args.dump_results and rank == 0:
