@@ -30,10 +30,13 @@ struct FlatInst {
     bool active, dec;
 };
 
-// Stage the next instance of the work list into lane tl (warp-uniform).  false when the
-// list is exhausted.
+// Claim and stage the next instance of the work list (warp-uniform): validate its rows,
+// rank them (MC-SF: stable counting sort on o~) and write the packed keys in policy order.
+// Instances outside the kernel's scope are appended to retry_list (k_mc_small runs them).
+// false when the list is exhausted.
 template <int POL, int NW>
-__device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, int *hist, FlatInst<NW> &L, int tl)
+__device__ __forceinline__ bool flat_stage(const KParams &P, uint32_t *keys, int *hist, long long &inst_out,
+                                           long long &off_out, int &n_out, int &M_out, int &a0_out)
 {
     const int lane = lane_id();
     const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
@@ -137,6 +140,25 @@ __device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, in
         }
         __threadfence_block();
         __syncwarp();
+        inst_out = inst;
+        off_out = off;
+        n_out = n;
+        M_out = M;
+        a0_out = a0;
+        return true;
+    }
+}
+
+// Stage the next instance of the work list into lane tl (warp-uniform).  false when the
+// list is exhausted.
+template <int POL, int NW>
+__device__ __forceinline__ bool flat_refill(const KParams &P, uint32_t *keys, int *hist, FlatInst<NW> &L, int tl)
+{
+    long long inst, off;
+    int n, M, a0;
+    if (!flat_stage<POL, NW>(P, keys, hist, inst, off, n, M, a0)) return false;
+    {
+        const int lane = lane_id();
         const uint32_t first = keys[off];
         const uint32_t second = n > 1 ? keys[off + 1] : 0u;
         if (lane == tl) {
@@ -294,6 +316,239 @@ __global__ void __launch_bounds__(128, 4) k_mc_flat(const KParams P)
             L.key = L.key2;
             if (L.h + 1 < L.n) L.key2 = keys[L.off + L.h + 1];
         }
+    }
+}
+
+
+// =======================================================================================
+// k_mc_flatq -- the same method with one instance per QUAD of lanes (8 per warp).
+//
+// k_mc_flat gives an instance one lane, so C2's 10^4 instances fill only ~1.7 warps per SM
+// and every admission is one lane's dependent chain over the whole 64-byte profile (issue
+// 25 %).  Here lane q of a quad holds profile words 4q..4q+3 (bytes tau = 16q+1 .. 16q+16):
+//   * Eq. 5 + the exact first fit: c and the prefix maximum F (first_fit) inside each lane's
+//     16 positions, then an exclusive max-scan of the lanes' maxima across the quad (two
+//     shuffles); F is written to the quad's 64 bytes of shared memory and the fixpoint
+//     D <- F(D + w) reads it (all four lanes, broadcast);
+//   * the ramp add is local (each lane its own words);
+//   * the profile shift by D bytes goes through the quad's 128-byte shared buffer (words
+//     16..31 stay zero): store four words, load five, funnel-shift;
+//   * the peak fold is local, max-reduced over the quad when the instance ends.
+// Staging is flat_stage (warp-cooperative, as in k_mc_flat); all four lanes of a quad run
+// the same instance, so quads diverge only between instances, as lanes did.
+// =======================================================================================
+template <int WPL>
+struct FlatQ {
+    uint32_t P[WPL];             // this lane's profile words
+    uint32_t key, key2;
+    const uint32_t *kp;          // keys of this instance, in policy order
+    long long inst, off, sumc, suma;
+    int t, n, M, h, maxc, dr, nr;
+    bool active, dec;
+};
+
+// group-local first fit (G lanes, WPL = 16 / G words each).  ql = lane within the group;
+// F = the group's 64 bytes.
+template <int G>
+__device__ __forceinline__ int flatq_first_fit(const uint32_t (&P)[16 / G], int L, int w, int ql, unsigned char *F,
+                                               uint32_t &pk16)
+{
+    constexpr int WPL = 16 / G;
+    const uint32_t b64 = 0x00400040u;
+    const uint32_t kL = (uint32_t)(64 - L) * 0x00010001u;
+    uint32_t pe_l[WPL], po_l[WPL], mw[WPL];
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) {
+        const int g = WPL * ql + i;                             // global word index
+        const uint32_t xe = __byte_perm(P[i], 0u, 0x4240);
+        const uint32_t xo = __byte_perm(P[i], 0u, 0x4341);
+        pk16 = __vimax3_s16x2_relu(pk16, xe, xo);
+        const uint32_t te = (uint32_t)(4 * g + 1) | ((uint32_t)(4 * g + 3) << 16);
+        const uint32_t to = te + 0x00010001u;
+        const uint32_t ce = add_fma(__viaddmin_s16x2(xe, kL, b64), te);
+        const uint32_t co = add_fma(__viaddmin_s16x2(xo, kL, b64), to);
+        const uint32_t t1 = __vimax_s16x2_relu(ce, co);
+        po_l[i] = __vimax_s16x2_relu(t1, __byte_perm(t1, 0u, 0x1010));
+        pe_l[i] = __vimax_s16x2_relu(ce, __byte_perm(po_l[i], 0u, 0x1044));
+        mw[i] = __byte_perm(po_l[i], 0u, 0x3232);
+    }
+    // exclusive prefix over the lane's words, then over the group's lanes
+    uint32_t ex[WPL];
+    uint32_t run = b64;
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) {
+        ex[i] = run;
+        run = __vimax_s16x2_relu(run, mw[i]);
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(KV_FULL, inc, d, G);
+        if (ql >= d) inc = __vimax_s16x2_relu(inc, y);
+    }
+    uint32_t before = __shfl_up_sync(KV_FULL, inc, 1, G);       // over lanes < ql
+    if (ql == 0) before = b64;
+    uint32_t fw[WPL];
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) {
+        const uint32_t r = __vimax_s16x2_relu(ex[i], before);
+        fw[i] = __byte_perm(__vimax_s16x2_relu(pe_l[i], r), __vimax_s16x2_relu(po_l[i], r), 0x6240);
+    }
+    if (WPL == 4) *reinterpret_cast<uint4 *>(F + 16 * ql) = make_uint4(fw[0], fw[1 % WPL], fw[2 % WPL], fw[3 % WPL]);
+    else if (WPL == 2) *reinterpret_cast<uint2 *>(F + 8 * ql) = make_uint2(fw[0], fw[1 % WPL]);
+    else *reinterpret_cast<uint32_t *>(F + 4 * ql) = fw[0];
+    __syncwarp();
+    int D = 0;
+    for (;;) {
+        const int x = min(D + w, 64) - 1;
+        const int f = (int)F[x] - 64;
+        if (f <= D) break;
+        D = f;
+    }
+    return D;
+}
+
+// P <- P shifted down by d bytes across the group (d <= 63; d = 0 is the identity); all
+// 32 lanes call it (no vote: on C2 nearly every step shifts)
+template <int G>
+__device__ __forceinline__ void flatq_shift(uint32_t (&P)[16 / G], int d, int ql, uint32_t *pbuf)
+{
+    constexpr int WPL = 16 / G;
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) pbuf[WPL * ql + i] = P[i];
+    __syncwarp();
+    const int w0 = WPL * ql + (d >> 2), sh = (d & 3) * 8;
+    uint32_t v[WPL + 1];
+#pragma unroll
+    for (int i = 0; i <= WPL; ++i) v[i] = pbuf[w0 + i];              // words >= 16 are zero
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) P[i] = __funnelshift_r(v[i], v[i + 1], sh);
+    __syncwarp();
+}
+
+// shared memory per warp: F bytes [32/G groups][64] (>= 256 bytes: also the staging
+// histogram), shift buffers [32/G][32 words]
+template <int G>
+__host__ __device__ constexpr int flatq_fbytes() { return (32 / G) * 64 > 256 ? (32 / G) * 64 : 256; }
+template <int G>
+__host__ __device__ constexpr int flatq_warp_bytes() { return flatq_fbytes<G>() + (32 / G) * 128; }
+
+template <int POL, int G>
+__global__ void __launch_bounds__(128) k_mc_flatq(const KParams P)
+{
+    constexpr int WPL = 16 / G, NG = 32 / G;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = lane / G, ql = lane % G;
+    unsigned char *wbase = smem_raw + (size_t)warp * flatq_warp_bytes<G>();
+    unsigned char *F = wbase + 64 * q;
+    uint32_t *pbuf = reinterpret_cast<uint32_t *>(wbase + flatq_fbytes<G>() + 128 * q);
+    int *hist = reinterpret_cast<int *>(wbase);                  // aliases F: staging only
+    uint32_t *keys = P.flat_keys;
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) pbuf[16 + WPL * ql + i] = 0u;    // zero tail of the shift buffer
+
+    // groups that take instances: all unless the grid has more warps than needed
+    uint32_t groups_l = KV_FULL;                                 // lanes of the groups in use
+    {
+        const long long n_work = P.work_list ? (long long)*P.work_count : P.n_inst;
+        const long long warps_total = (long long)gridDim.x * (blockDim.x >> 5);
+        const long long gpw = (n_work + warps_total - 1) / warps_total;
+        if (gpw < NG) groups_l = gpw < 1 ? ((1u << G) - 1u) : (uint32_t)((1ull << (G * gpw)) - 1ull);
+    }
+
+    FlatQ<WPL> L;
+    L.active = false;
+    uint32_t pk16 = 0u;
+    bool more = true;
+    __syncwarp();
+    for (;;) {
+        // idle groups: bit G*k set for group k
+        uint32_t idle = __ballot_sync(KV_FULL, !L.active && ql == 0) & groups_l;
+        while (idle && more) {
+            const int tq = (__ffs(idle) - 1) / G;
+            long long inst, off;
+            int n, M, a0;
+            more = flat_stage<POL, 16>(P, keys, hist, inst, off, n, M, a0);
+            if (more && q == tq) {
+#pragma unroll
+                for (int i = 0; i < WPL; ++i) L.P[i] = 0u;
+                L.kp = keys + off;
+                L.key = L.kp[0];
+                L.key2 = n > 1 ? L.kp[1] : 0u;
+                L.inst = inst;
+                L.off = off;
+                L.sumc = 0;
+                L.suma = (long long)a0 * n;
+                L.t = a0;
+                L.n = n;
+                L.M = M;
+                L.h = 0;
+                L.maxc = -1;
+                L.dr = L.nr = 0;
+                L.active = true;
+                L.dec = false;
+                pk16 = 0u;
+            }
+            idle &= idle - 1;
+            __syncwarp();
+        }
+        if (!__any_sync(KV_FULL, L.active)) break;
+
+        // instances whose every request is admitted: drain S, write the results
+        const bool drain = L.active && L.h == L.n;
+        if (__any_sync(KV_FULL, drain)) {
+            uint32_t pk = max_bytes16(L.P, pk16);
+#pragma unroll
+            for (int d = 1; d < G; d <<= 1) pk = __vimax_s16x2_relu(pk, __shfl_xor_sync(KV_FULL, pk, d));
+            if (drain) {
+                if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
+                else L.nr += max(0, L.maxc - L.t);
+                if (ql == 0) {
+                    if (P.tel) P.tel[L.inst] = L.sumc - L.suma;
+                    if (P.rounds) P.rounds[L.inst] = (long long)(L.dr + L.nr);
+                    if (P.drounds) P.drounds[L.inst] = (long long)L.dr;
+                    if (P.evictions) P.evictions[L.inst] = 0;
+                    if (P.makespan) P.makespan[L.inst] = L.maxc;
+                    if (P.peak) P.peak[L.inst] = hmax16(pk);
+                    if (P.status) P.status[L.inst] = ST_OK;
+                }
+                L.active = false;
+            }
+        }
+
+        // Eq. 5 for the head at this round and, if it fails, the first round it holds
+        // (every group computes; only active ones use it)
+        const bool go = L.active;
+        const int w = (int)(L.key & 63u), s = (int)((L.key >> 6) & 63u);
+        const int D = flatq_first_fit<G>(L.P, (go ? L.M : 64) - s, go ? w : 1, ql, F, pk16);
+        const int jump = go ? D : 0;
+        flatq_shift<G>(L.P, jump, ql, pbuf);
+        if (go) {
+            L.dr += D;
+            if (jump > 0) L.t += jump;
+            // admission at the landing round: p = t, c = t + o (Eq. 3)
+            const int idx = (int)(L.key >> 12);
+            L.dec = true;
+            const uint32_t S4 = rep4(s);
+            const uint32_t Kw = rep4(127 - w);
+#pragma unroll
+            for (int i = 0; i < WPL; ++i) {
+                const uint32_t tw = tau_word(0) + (uint32_t)(4 * (WPL * ql + i)) * 0x01010101u;
+                L.P[i] = add_fma(L.P[i], add_fma(S4, tw) & ~sign_bytes(Kw + tw));
+            }
+            const int c = L.t + w;
+            if (ql == 0) {
+                if (P.start) P.start[L.off + idx] = L.t;
+                if (P.completion) P.completion[L.off + idx] = c;
+            }
+            L.sumc += c;
+            L.maxc = max(L.maxc, c);
+            ++L.h;
+            L.key = L.key2;
+            if (L.h + 1 < L.n) L.key2 = L.kp[L.h + 1];
+        }
+        __syncwarp();
     }
 }
 

@@ -436,6 +436,34 @@ int launch_flat(sched_ctx *c, K kernel, const KParams &P, const char *name)
     return SCHED_OK;
 }
 
+// k_mc_flatq<POL, G>: one instance per group of G lanes (32/G per warp), 4 warps per block;
+// enough warps for one instance per group
+template <int G, typename K>
+int launch_flatq(sched_ctx *c, K kernel, const KParams &P, const char *name)
+{
+    const long long warps = (P.n_inst + (32 / G) - 1) / (32 / G);
+    const int block = 128, smem = 4 * flatq_warp_bytes<G>();
+    CUDA_TRY(c, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int grid = 1;
+    int rc = occupancy_grid(c, kernel, block, smem, warps, &grid);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+        e0 = take_event(c);
+        e1 = take_event(c);
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    }
+    kernel<<<grid, block, smem, c->stream>>>(P);
+    CUDA_TRY(c, cudaGetLastError());
+    if (c->timing) {
+        CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+        c->pending.push_back({e0, e1, name});
+    }
+    c->launches++;
+    c->sim_launches++;
+    return SCHED_OK;
+}
+
 int check_common(sched_ctx *c, const sched_instances *inst)
 {
     if (!c) return SCHED_E_STATE;
@@ -667,7 +695,20 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 int r;
 #define KV_FLAT(NWV) (sf ? launch_flat(c, k_mc_flat<POL_MCSF, NWV>, F, "k_mc_flat<MCSF>")                 \
                          : launch_flat(c, k_mc_flat<POL_MCBENCH, NWV>, F, "k_mc_flat<MCBENCH>"))
-                r = fnw == 4 ? KV_FLAT(4) : fnw == 8 ? KV_FLAT(8) : fnw == 13 ? KV_FLAT(13) : KV_FLAT(16);
+                // one instance per quad of lanes (k_mc_flatq); KVSCHED_FLAT_LANE=1 keeps one
+                // lane per instance (k_mc_flat, A/B only)
+                const char *fl_env = getenv("KVSCHED_FLAT_LANE");
+                if (fl_env && fl_env[0] == '1')
+                    r = fnw == 4 ? KV_FLAT(4) : fnw == 8 ? KV_FLAT(8) : fnw == 13 ? KV_FLAT(13) : KV_FLAT(16);
+                else if (fl_env && fl_env[0] == '4')
+                    r = sf ? launch_flatq<4>(c, k_mc_flatq<POL_MCSF, 4>, F, "k_mc_flatq<MCSF>")
+                           : launch_flatq<4>(c, k_mc_flatq<POL_MCBENCH, 4>, F, "k_mc_flatq<MCBENCH>");
+                else if (fl_env && fl_env[0] == '2')
+                    r = sf ? launch_flatq<16>(c, k_mc_flatq<POL_MCSF, 16>, F, "k_mc_flatq<MCSF>")
+                           : launch_flatq<16>(c, k_mc_flatq<POL_MCBENCH, 16>, F, "k_mc_flatq<MCBENCH>");
+                else
+                    r = sf ? launch_flatq<8>(c, k_mc_flatq<POL_MCSF, 8>, F, "k_mc_flatq<MCSF>")
+                           : launch_flatq<8>(c, k_mc_flatq<POL_MCBENCH, 8>, F, "k_mc_flatq<MCBENCH>");
 #undef KV_FLAT
                 if (r) return r;
                 KParams C = A;
