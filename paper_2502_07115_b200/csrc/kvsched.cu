@@ -1469,7 +1469,7 @@ int sched_finalize(sched_ctx *c)
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
         for (DevBuf *b : {&c->counter, &c->bounds, &c->rq, &c->arank, &c->pstart, &c->relnext, &c->total, &c->retry, &c->scan, &c->dec, &c->h_pk, &c->comp, &c->fkeys, &c->h_off,
-                          &c->h_req, &c->h_mem, &c->h_out})
+                          &c->h_req, &c->h_mem, &c->h_out, &c->rq8, &c->arr8, &c->capv, &c->lpt})
             if (b->p) cudaFree(b->p);
         for (auto &p : c->pending) {
             cudaEventDestroy(p.e0);
@@ -1478,7 +1478,8 @@ int sched_finalize(sched_ctx *c)
         for (auto e : c->free_events) cudaEventDestroy(e);
         for (auto e : c->chunk_events) cudaEventDestroy(e);
         for (auto &r : c->extra) {
-            for (DevBuf *b : {&r.counter, &r.bounds, &r.rq, &r.arank, &r.pstart, &r.relnext, &r.retry, &r.comp, &r.fkeys})
+            for (DevBuf *b : {&r.counter, &r.bounds, &r.rq, &r.arank, &r.pstart, &r.relnext, &r.retry, &r.comp, &r.fkeys,
+                              &r.rq8, &r.arr8, &r.capv, &r.lpt})
                 if (b->p) cudaFree(b->p);
             if (r.stream) cudaStreamDestroy(r.stream);
         }
