@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--dump-results", default="",
                     help="rank 0 saves the gathered per-instance (TEL, rounds, status) rows of the "
                          "last step here (.npy; tests compare 1-rank and N-rank runs)")
-    ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta", "mcsf_protected"])
+    ap.add_argument("--policy", default="mcsf", choices=["mcsf", "mcbench", "alpha", "alpha_beta", "mcsf_protected",
+                                                          "mcsf_protected_raise"])
     ap.add_argument("--eps", type=float, default=0.2, help="prediction noise for mcsf_protected (P:519)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -112,8 +113,8 @@ def policy_of(K, name):
         return K.Policy("alpha", (1, 4))
     if name == "alpha_beta":
         return K.Policy("alpha_beta", (1, 5), W.beta_threshold(0.1), seed=1)
-    if name == "mcsf_protected":
-        return K.Policy("mcsf_protected", (1, 10))
+    if name in ("mcsf_protected", "mcsf_protected_raise"):
+        return K.Policy(name, (1, 10))
     return K.Policy(name)
 
 
@@ -122,7 +123,8 @@ def oracle_policy(name):
     return {"mcsf": (oracle.MCSF, {}), "mcbench": (oracle.MCBENCH, {}),
             "alpha": (oracle.ALPHA, dict(alpha=(1, 4))),
             "alpha_beta": (oracle.ALPHA_BETA, dict(alpha=(1, 5), beta_thresh=W.beta_threshold(0.1), seed=1)),
-            "mcsf_protected": (oracle.MCSF_PROT, dict(alpha=(1, 10)))}[name]
+            "mcsf_protected": (oracle.MCSF_PROT, dict(alpha=(1, 10))),
+            "mcsf_protected_raise": (oracle.MCSF_PROT_RAISE, dict(alpha=(1, 10)))}[name]
 
 
 def cpu_oracle_rate(batch, policy: str, seconds: float, gid0: int = 0, nthreads: int = 0):
@@ -240,7 +242,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     (batch, _), cfg = make_workload(args.workload, args.instances, 0)
-    if args.policy == "mcsf_protected":
+    if args.policy.startswith("mcsf_protected"):
         batch = W.with_prediction_noise(batch, args.eps, seed=7)
         cfg["prediction_noise_eps"] = args.eps
     per_step = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.5)
@@ -287,7 +289,7 @@ def main():
             dist.init_process_group(backend)
 
     (batch, id0), cfg = make_workload(args.workload, args.instances, rank, world, args.split)
-    if args.policy == "mcsf_protected":
+    if args.policy.startswith("mcsf_protected"):
         batch = W.with_prediction_noise(batch, args.eps, seed=7 + rank)
         cfg["prediction_noise_eps"] = args.eps
     hints = K.hints_of(batch)

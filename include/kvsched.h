@@ -28,6 +28,11 @@
  *                     is cleared with probability beta, in whole passes until the batch fits
  *                     (DESIGN Q14); draws are Philox4x32-10 on (t, pass, idx, 0) keyed by
  *                     seed ^ (gid * 0x9E3779B97F4A7C15).
+ *   SCHED_MCSF_PROTECTED_RAISE  the same, except that a cleared request re-enters the queue
+ *                     with its prediction raised to the tokens it is known to need,
+ *                     max(o~, t - p + 1) for a request started at p and cleared at t
+ *                     (DESIGN Q26b); instances with more than 3 x 1024 requests, or whose
+ *                     rerun needs the full ring, are UNSUPPORTED.
  *   SCHED_MCSF_PROTECTED  MC-SF under prediction error: Algorithm 1 with the
  *                     possibly wrong predictions o~ against the budget floor((1-alpha)M); when
  *                     the realised occupancy of a batch exceeds M every active request is
@@ -71,7 +76,8 @@ enum {
 };
 
 /* policies (see above) */
-enum { SCHED_MCSF = 0, SCHED_MC_BENCH = 1, SCHED_ALPHA = 2, SCHED_ALPHA_BETA = 3, SCHED_MCSF_PROTECTED = 4 };
+enum { SCHED_MCSF = 0, SCHED_MC_BENCH = 1, SCHED_ALPHA = 2, SCHED_ALPHA_BETA = 3, SCHED_MCSF_PROTECTED = 4,
+       SCHED_MCSF_PROTECTED_RAISE = 5 };
 
 /* per-instance status */
 enum {
@@ -137,7 +143,7 @@ enum { SCHED_REQ_I32X4 = 0, SCHED_REQ_U16X4_DELTA = 1, SCHED_REQ_U8X4_DELTA = 2,
  * Instances that exceed a caller-given bound get status SCHED_INST_UNSUPPORTED.            */
 
 typedef struct {
-    int32_t policy;             /* SCHED_MCSF .. SCHED_MCSF_PROTECTED                        */
+    int32_t policy;             /* SCHED_MCSF .. SCHED_MCSF_PROTECTED_RAISE                  */
     int32_t alpha_num;          /* alpha = alpha_num / alpha_den in [0, 1) (alpha policies and
                                    SCHED_MCSF_PROTECTED);                                   */
     int32_t alpha_den;          /*   budget B = ((den - num) * M) / den (DESIGN Q15)         */

@@ -43,7 +43,11 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
     const int *reqi = reinterpret_cast<const int *>(P.req);
     InstResult res{0, 0, 0, 0, 0, 0, ST_OK};
 
-    bool bad = false, unsup = n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows;
+    // DESIGN Q26b: a cleared request's prediction is raised to the tokens it is known to need
+    // and the instance is re-ranked (keys sorted in the ring area, which a clearing resets)
+    const bool raise = P.policy == POL_MCSF_PROT_RAISE;
+    bool bad = false, unsup = n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows ||
+                              (raise && next_pow2(max(n, 2)) > 3 * L);
     long long suma = 0, sumo = 0;
     if (!unsup) {
         for (int k = lane; k < n; k += 32) {
@@ -73,8 +77,12 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
     for (int i = lane; i < L; i += 32) { S.pp[i] = 0; S.pa[i] = 0; S.rel[i] = -1; }
     for (int w = lane; w < nw; w += 32) { S.bm[w] = 0u; S.infl[w] = 0u; }
     S.sm[lane] = 0u;
-    __syncwarp();
     WarpQueue Q{S.bm, S.sm, (nw + 31) >> 5};
+    uint4 *rqw = const_cast<uint4 *>(P.rq) + off;           // Q26b rewrites the ranks
+    int *arw = const_cast<int *>(P.arank) + off;
+    if (raise)
+        for (int k = lane; k < n; k += 32) P.pstart[off + k] = -1;   // -1 = not in S, not completed
+    __syncwarp();
 
     const long long cap64 = P.round_cap > 0 ? P.round_cap : default_cap(reqi[(off + n - 1) * 4], sumo);
     const int cap = (int)min(cap64, 0x7ffffffell);
@@ -207,7 +215,14 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
                         ev += __popc(am);
                         sumc -= warp_sum_i64(act ? (long long)(pst[j] + reqi[(off + j) * 4 + 2]) : 0ll);
                         if (act) {
-                            q_insert(Q, (int)P.arank[off + j]);
+                            const int rj = arw[j];
+                            if (raise) {
+                                // ran rounds p..t-1, unfinished (c > t): o >= t - p + 1 (Q26b)
+                                const int need = t - pst[j] + 1;
+                                if ((int)rqw[rj].y < need) rqw[rj].y = (uint32_t)need;
+                                pst[j] = -1;
+                            }
+                            q_insert(Q, rj);
                             if (P.completion) P.completion[off + j] = -1;
                             if (P.start) P.start[off + j] = -1;
                         }
@@ -215,8 +230,45 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
                 }
                 if (wi < nw) S.infl[wi] = 0u;
             }
-            // the head is a rank: recompute it over the re-queued set
             __syncwarp();
+            if (raise) {
+                // re-rank by (o~, idx) with the raised predictions: keys in the ring area
+                __threadfence_block();
+                __syncwarp();
+                uint32_t *keys = reinterpret_cast<uint32_t *>(S.pp);   // pp, pa, rel: 3L words
+                const int NPk = next_pow2(max(n, 2));
+                for (int k = lane; k < NPk; k += 32)
+                    keys[k] = k < n ? (((uint32_t)min((int)rqw[arw[k]].y, 0x1ffff) << 15) | (uint32_t)k) : 0xffffffffu;
+                __syncwarp();
+                for (int kk = 2; kk <= NPk; kk <<= 1) {
+                    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                        for (int i = lane; i < (NPk >> 1); i += 32) {
+                            const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
+                            const int hi = lo + jj;
+                            const bool up = (lo & kk) == 0;
+                            const uint32_t x = keys[lo], y = keys[hi];
+                            if ((x > y) == up) { keys[lo] = y; keys[hi] = x; }
+                        }
+                        __syncwarp();
+                    }
+                }
+                for (int r = lane; r < n; r += 32) {
+                    const int idx = (int)(keys[r] & 0x7fffu);
+                    const int4 q = P.req[off + idx];
+                    rqw[r] = make_uint4((uint32_t)q.y, keys[r] >> 15, (uint32_t)q.z, (uint32_t)idx);
+                    arw[idx] = r;
+                }
+                __threadfence_block();
+                __syncwarp();
+                // the waiting queue: every arrived request not in S and not completed
+                for (int w = lane; w < nw; w += 32) S.bm[w] = 0u;
+                S.sm[lane] = 0u;
+                __syncwarp();
+                for (int k = lane; k < next; k += 32)
+                    if (pst[k] < 0) q_insert(Q, arw[k]);
+                __syncwarp();
+            }
+            // the head is a rank: recompute it over the re-queued set
             h = q_first(Q);
             hstale = h != KV_INF;
             for (int i = lane; i < L; i += 32) { S.pp[i] = 0; S.pa[i] = 0; S.rel[i] = -1; }
@@ -224,7 +276,7 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
             Ga.used = 0u;
             __syncwarp();
             evictions += ev;
-            cycle = next == n && next_at_clear == next && ev == adm_since_clear;
+            cycle = !raise && next == n && next_at_clear == next && ev == adm_since_clear;
             next_at_clear = next;
             adm_since_clear = 0;
         }
@@ -285,6 +337,13 @@ __device__ void prot_instance(const KParams &P, long long inst, const ProtSmem &
         }
     }
 
+    if (status == ST_RETRY && raise) {
+        // the re-ranks have rewritten this instance's entries, so it cannot restart on the
+        // full ring: UNSUPPORTED (documented in kvsched.h)
+        fill_unscheduled(P, off, n);
+        write_result(P, inst, InstResult{0, 0, 0, 0, 0, 0, ST_UNSUPPORTED});
+        return;
+    }
     if (status == ST_RETRY) {
         if (lane == 0) P.retry_list[atomicAdd(P.retry_count, 1ull)] = inst;
         return;

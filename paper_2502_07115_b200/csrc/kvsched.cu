@@ -488,7 +488,7 @@ int check_common(sched_ctx *c, const sched_instances *inst)
 int check_policy(sched_ctx *c, const sched_policy *pol)
 {
     if (!pol) return fail(c, SCHED_E_ARG, "pol is NULL");
-    if (pol->policy < SCHED_MCSF || pol->policy > SCHED_MCSF_PROTECTED)
+    if (pol->policy < SCHED_MCSF || pol->policy > SCHED_MCSF_PROTECTED_RAISE)
         return fail(c, SCHED_E_ARG, "unknown policy %d", pol->policy);
     if (pol->flags & ~(SCHED_FLAG_PER_ROUND | SCHED_FLAG_WARP_PER_INSTANCE))
         return fail(c, SCHED_E_ARG, "unknown flags 0x%x", pol->flags);
@@ -761,14 +761,14 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     const int L_full = next_pow2(max_len + 33);
     // the protected kernel keeps three per-warp rings: a 1024-slot window doubles its
     // occupancy (measured 1.48x faster on C4 with eps = 0.2 than 2048, 512 is slower)
-    int ring_short = pol->policy == SCHED_MCSF_PROTECTED ? KV_PROT_SHORT : KV_RING_SHORT;   // KVSCHED_RING_WINDOW: experiments only
+    int ring_short = pol->policy >= SCHED_MCSF_PROTECTED ? KV_PROT_SHORT : KV_RING_SHORT;   // KVSCHED_RING_WINDOW: experiments only
     if (const char *e = getenv("KVSCHED_RING_WINDOW")) {
         const int v = atoi(e);
         if (v >= 64 && (v & (v - 1)) == 0) ring_short = v;
     }
     const int L_short = L_full < ring_short ? L_full : ring_short;
     P.L = L_short;
-    const bool prot = pol->policy == SCHED_MCSF_PROTECTED;
+    const bool prot = pol->policy >= SCHED_MCSF_PROTECTED;
     // MC policies with M <= 32767: the 16-bit profile ring with staged arrivals
     // (kernel_mcring.cuh); KVSCHED_OLD_RING=1 keeps the 32-bit k_ring (A/B only)
     const char *old_ring = getenv("KVSCHED_OLD_RING");
@@ -936,6 +936,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         case SCHED_MC_BENCH: name = "k_ring<MCBENCH>"; return launch_sim(c, k_ring<POL_MCBENCH>, Q, Q.warp_bytes, name);
         case SCHED_ALPHA: name = "k_ring<ALPHA>"; return launch_sim(c, k_ring<POL_ALPHA>, Q, Q.warp_bytes, name);
         case SCHED_MCSF_PROTECTED: name = "k_prot<MCSF_PROTECTED>"; return launch_sim(c, k_prot, Q, Q.warp_bytes, name);
+        case SCHED_MCSF_PROTECTED_RAISE: name = "k_prot<MCSF_PROTECTED_RAISE>"; return launch_sim(c, k_prot, Q, Q.warp_bytes, name);
         default: name = "k_ring<ALPHA_BETA>"; return launch_sim(c, k_ring<POL_ALPHA_BETA>, Q, Q.warp_bytes, name);
         }
     };

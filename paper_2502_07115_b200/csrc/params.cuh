@@ -5,7 +5,7 @@
 
 namespace kv {
 
-enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3, POL_MCSF_PROT = 4 };
+enum { POL_MCSF = 0, POL_MCBENCH = 1, POL_ALPHA = 2, POL_ALPHA_BETA = 3, POL_MCSF_PROT = 4, POL_MCSF_PROT_RAISE = 5 };
 enum { ST_OK = 0, ST_INVALID = 1, ST_LIVELOCK = 2, ST_UNSUPPORTED = 3, ST_RETRY = 4 /* internal */ };
 
 struct KParams {

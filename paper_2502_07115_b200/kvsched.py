@@ -15,9 +15,9 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libkvsched.so"
 
-MCSF, MC_BENCH, ALPHA, ALPHA_BETA, MCSF_PROTECTED = 0, 1, 2, 3, 4
+MCSF, MC_BENCH, ALPHA, ALPHA_BETA, MCSF_PROTECTED, MCSF_PROTECTED_RAISE = 0, 1, 2, 3, 4, 5
 POLICY_IDS = {"mcsf": MCSF, "mcbench": MC_BENCH, "alpha": ALPHA, "alpha_beta": ALPHA_BETA,
-              "mcsf_protected": MCSF_PROTECTED}
+              "mcsf_protected": MCSF_PROTECTED, "mcsf_protected_raise": MCSF_PROTECTED_RAISE}
 INST_OK, INST_INVALID, INST_LIVELOCK, INST_UNSUPPORTED = 0, 1, 2, 3
 FLAG_PER_ROUND = 1
 FLAG_WARP_PER_INSTANCE = 2

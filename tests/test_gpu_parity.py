@@ -15,7 +15,7 @@ import workloads as W
 pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-KIND = {0: "mcsf", 1: "mcbench", 2: "alpha", 3: "alpha_beta", 4: "mcsf_protected"}
+KIND = {0: "mcsf", 1: "mcbench", 2: "alpha", 3: "alpha_beta", 4: "mcsf_protected", 5: "mcsf_protected_raise"}
 
 
 @pytest.fixture(scope="module")
@@ -759,7 +759,7 @@ R2 = json.loads((GOLDEN / "round2_pins.json").read_text())
 
 @pytest.mark.parametrize("case", R2["cases"], ids=lambda c: c["name"])
 def test_round2_worked_examples_on_gpu(K, ctx, oracle_mod, case):
-    pol = {"alpha": 2, "alpha_beta": 3, "mcsf_prot": 4}[case["policy"]]
+    pol = {"alpha": 2, "alpha_beta": 3, "mcsf_prot": 4, "mcsf_prot_raise": 5}[case["policy"]]
     b = W.from_instances([(case["req"], case["M"])])
     o, g = check(K, ctx, oracle_mod, b, pol, case["name"], alpha=tuple(case["alpha"]),
                  beta_thresh=case.get("beta_thresh", 0), seed=case.get("seed", 0),
@@ -867,3 +867,18 @@ def test_c4_full_config_mcsf(K, ctx, oracle_mod):
     launch, every output of every instance against the oracle."""
     b = W.c4(100_000, 4)
     check(K, ctx, oracle_mod, b, 0, "C4 10^5 MC-SF")
+
+
+# ---------------------------------------------------------------------------------------
+# DESIGN Q26b: protected MC-SF whose cleared requests re-enter with raised predictions
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", ["small", "c4"])
+@pytest.mark.parametrize("eps", [0.2, 0.8])
+@pytest.mark.parametrize("flags", [0, 1])
+def test_protected_raise(K, ctx, oracle_mod, shape, eps, flags):
+    b = {"small": lambda: W.random_small(2000, 140, n_max=40, M_lo=10, M_hi=90, a_max=30),
+         "c4": lambda: W.c4(48, 141)}[shape]()
+    b = W.with_prediction_noise(b, eps, seed=13)
+    o, g = check(K, ctx, oracle_mod, b, 5, f"Q26b {shape} eps={eps}", alpha=(1, 10), flags=flags)
+    assert o["evictions"].sum() > 0
+    assert (o["status"] == 0).sum() > 0

@@ -482,7 +482,7 @@ def test_wallclock_unit_clock_is_tel(oracle_mod):
 # Round 2: eviction policies against hand-worked cases and an independent literal re-run
 # ----------------------------------------------------------------------------------------
 R2 = json.loads((GOLDEN / "round2_pins.json").read_text())
-POL2 = dict(POL, mcsf_prot=4)
+POL2 = dict(POL, mcsf_prot=4, mcsf_prot_raise=5)
 
 
 @pytest.mark.parametrize("case", R2["cases"], ids=lambda c: c["name"])
