@@ -2,7 +2,7 @@
 """Run every BASELINE.json config through the GPU path (C ABI), check sampled instances
 against the CPU oracle, and report throughput plus the statistic the config is quoted for.
 
-    python tools/configs_report.py [--out profiles/r01/configs_report.json] [--quick]
+    python tests/tools/configs_report.py [--out profiles/r01/configs_report.json] [--quick]
 
 C1  tiny (n=8, M=16): MC-SF TEL vs the brute-force hindsight optimum (Eqs. 1-4)
 C2  AM1 (n=1000 at t=0, M=40): TEL(MC-SF) / LB_sorted, an upper bound on the ratio to OPT
@@ -21,7 +21,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 import oracle  # noqa: E402  (test infrastructure: parity sampling and OPT only)
@@ -29,7 +29,22 @@ import paper_2502_07115_b200 as K  # noqa: E402
 import workloads as W  # noqa: E402
 
 POL = {"mcsf": oracle.MCSF, "mcbench": oracle.MCBENCH, "alpha": oracle.ALPHA, "alpha_beta": oracle.ALPHA_BETA,
-       "mcsf_protected": oracle.MCSF_PROT}
+       "mcsf_protected": oracle.MCSF_PROT, "mcsf_protected_raise": oracle.MCSF_PROT_RAISE}
+
+
+def oracle_rate(b, kind, seconds=4.0, **kw):
+    """The oracle on all host cores over a bounded prefix of the batch (rounds/s)."""
+    import os
+    chunk, k, busy, rounds, insts = max(1, min(b.n_inst, 500)), 0, 0.0, 0, 0
+    while busy < seconds and k < b.n_inst:
+        sub_ = b.slice(k, min(k + chunk, b.n_inst))
+        t0 = time.perf_counter()
+        o = oracle.simulate_batch(sub_.offset, sub_.req, sub_.mem, POL[kind], gid0=k, **kw)
+        busy += time.perf_counter() - t0
+        rounds += int(o["rounds"][o["status"] == 0].sum())
+        insts += sub_.n_inst
+        k += chunk
+    return {"rounds_per_s": rounds / busy, "cores": os.cpu_count(), "sample_instances": insts}
 
 
 def gpu(ctx, b, policy, reps=3):
@@ -84,7 +99,7 @@ def summarize(b, g, ms, kname):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r01" / "configs_report.json"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r02" / "configs_report.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     q = a.quick
@@ -106,6 +121,7 @@ def main():
     r["tel_over_opt"] = {"n": len(ratios), "mean": float(np.mean(ratios)), "max": float(np.max(ratios)),
                          "exact_optimum": int(n_opt), "never_below_opt": bool(min(ratios) >= 1.0)}
     r["parity"] = sample_parity(b, g, pol, "mcsf", 2000)
+    r["oracle"] = oracle_rate(b, "mcsf")
     report["C1"] = r
     print("C1", json.dumps(r), f"({time.time() - t0:.0f}s)", flush=True)
 
@@ -125,18 +141,20 @@ def main():
                                "lb_parity_sampled": int(sum(lb[k] == oracle.lb_sorted(*b.instance(k))
                                                             for k in range(64)))}
     r["parity"] = sample_parity(b, g, pol, "mcsf", 64)
+    r["oracle"] = oracle_rate(b, "mcsf")
     report["C2"] = r
     print("C2", json.dumps(r), flush=True)
 
     # C3: trace-shaped n=10^4, both demand levels
     for lam in (0.4, 2.0):
-        b = W.c3(256 if q else 2048, 3, lam)
+        b = W.c3(256 if q else 4096, 3, lam)
         for kind in ("mcsf", "mcbench"):
             g, ms, kn = gpu(ctx, b, K.Policy(kind), reps=1)
             r = summarize(b, g, ms, kn)
             ok = g["status"] == 0
             r["avg_latency_rounds"] = float(g["tel"][ok].sum() / (b.n_req / b.n_inst * ok.sum()))
-            r["parity"] = sample_parity(b, g, K.Policy(kind), kind, 4)
+            r["parity"] = sample_parity(b, g, K.Policy(kind), kind, 16)
+            r["oracle"] = oracle_rate(b, kind)
             report[f"C3 lambda={lam} {kind}"] = r
             print("C3", lam, kind, json.dumps(r), flush=True)
 
@@ -152,8 +170,24 @@ def main():
                                    "min": float(lat.min()), "livelock": int((g["status"] == 2).sum())}
         r["evictions_total"] = int(g["evictions"].sum())
         r["parity"] = sample_parity(b, g, pol, kind, 32)
+        r["oracle"] = oracle_rate(b, kind, alpha=pol.alpha, beta_thresh=pol.beta_thresh, seed=pol.seed)
         report[f"C4 {name}"] = r
         print("C4", name, json.dumps(r), flush=True)
+
+    # NEXT-1: prediction noise, protected MC-SF (alpha = 0.1) under Q26 and Q26b
+    bn = W.c4(2000 if q else 20_000, 4)
+    for eps in (0.2, 0.5, 0.8):
+        nb = W.with_prediction_noise(bn, eps, seed=7)
+        for kind in ("mcsf_protected", "mcsf_protected_raise"):
+            pol = K.Policy(kind, (1, 10))
+            g, ms, kn = gpu(ctx, nb, pol, reps=1)
+            r = summarize(nb, g, ms, kn)
+            ok = g["status"] == 0
+            r["avg_latency_rounds"] = float((g["tel"][ok] / 1000.0).mean()) if ok.any() else None
+            r["completed"] = int(ok.sum())
+            r["parity"] = sample_parity(nb, g, pol, kind, 16)
+            report[f"C4 noise eps={eps} {kind}"] = r
+            print("C4noise", eps, kind, json.dumps(r), flush=True)
 
     # NEXT-4: wall clock of the C4 MC-SF and MC-Benchmark schedules under an affine batch time
     # (placeholder constants: 20 ms per batch + 0.05 ms per token; only ratios are claimed)
@@ -186,6 +220,7 @@ def main():
     g, ms, kn = gpu(ctx, b, pol)
     r = summarize(b, g, ms, kn)
     r["parity"] = sample_parity(b, g, pol, "mcsf", 500)
+    r["oracle"] = oracle_rate(b, "mcsf")
     report["C5"] = r
     print("C5", json.dumps(r), flush=True)
 

@@ -1,7 +1,7 @@
 # Long randomized parity sweep (GPU box): many seeded batches of mixed shapes through every
 # policy, flag and size hint of the C ABI, each compared element by element with the oracle.
 # Not part of the pytest suite (it runs for minutes); the log goes to gpurun_out/fuzz_parity.log.
-#   python scripts/fuzz_parity.py [minutes]
+#   python tests/tools/fuzz_parity.py [minutes]
 import sys
 import time
 

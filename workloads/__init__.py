@@ -195,6 +195,24 @@ def am1_paper(n_inst: int, seed: int = 20) -> Batch:
                      dict(seed=seed))
 
 
+def am2_paper(n_inst: int, seed: int = 21) -> Batch:
+    """The paper's own AM2 draw (P:408): per trial M~U{30..50}, T~U{40..60}, lambda~U[0.5, 1.5];
+    Poisson(lambda) arrivals on each round 1..T (DESIGN Q20); s~U{1..5}; o~U{1..M-s}."""
+    g = _rng([21, seed])
+    M = g.integers(30, 51, size=n_inst)
+    T = g.integers(40, 61, size=n_inst)
+    lam = g.uniform(0.5, 1.5, size=n_inst)
+    counts = g.poisson(lam[:, None], size=(n_inst, 60))
+    counts[np.arange(60)[None, :] >= T[:, None]] = 0
+    sizes = counts.sum(axis=1).astype(np.int64)
+    rounds = np.broadcast_to(np.arange(1, 61, dtype=np.int64), (n_inst, 60))
+    a = np.repeat(rounds.ravel(), counts.ravel())
+    Mrep = np.repeat(M, sizes)
+    s = g.integers(1, 6, size=a.shape[0])
+    o = g.integers(1, Mrep - s + 1)
+    return _assemble(a, s, o, sizes, M, "AM2-paper", dict(seed=seed))
+
+
 def am2(n_inst: int, seed: int = 5, lambdas=C5_LAMBDAS, Ms=C5_MS, id0: int = 0) -> Batch:
     """C5 (Arrival Model 2): instance k sits on grid cell (k+id0) mod |grid| of
     lambda x M; T~U{40..60}; Poisson(lambda) arrivals on each round 1..T (DESIGN Q20);
