@@ -78,29 +78,43 @@ struct LaneInst {                            // one lane's instance (registers)
 // reports): decided from the CSR offsets and budgets alone, before any row is read.
 __device__ __forceinline__ bool lane_size_ok(const KParams &P, int n, int M)
 {
-    return n >= 1 && n <= LANE_NP && M <= 64 && n <= P.max_requests && M <= P.max_mem;
+    return n >= 1 && n <= (P.lane_max_n > 0 ? P.lane_max_n : LANE_NP) && M <= 64 && n <= P.max_requests &&
+           M <= P.max_mem;
 }
 
 // Lists the instances outside the size scope (retry_list / retry_count of the KParams it is
 // given) so that k_mc_small can run them beside k_mc_lane; one thread per instance,
 // warp-aggregated appends.
-__global__ void k_lane_split(const KParams P)
+// With `other` set, an out-of-scope instance whose first and last arrivals differ (it can
+// never run on k_mc_flat, which takes simultaneous arrivals) goes to `other` / `other_count`
+// instead, so the flat kernel does not stage it only to reject it.
+__global__ void k_lane_split(const KParams P, long long *other, unsigned long long *other_count)
 {
     const long long stride = (long long)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     for (long long k0 = blockIdx.x * (long long)blockDim.x; k0 < P.n_inst; k0 += stride) {
         const long long k = k0 + threadIdx.x;
-        bool out = false;
+        bool out = false, flat = false;
         if (k < P.n_inst) {
             const long long n = P.offset[k + 1] - P.offset[k];
             out = !lane_size_ok(P, n > 0x7fffffffll ? 0x7fffffff : (int)n, P.mem[k]);
+            if (out) {
+                const long long off = P.offset[k] - P.row_base;
+                flat = !other || (n > 0 && P.req[off].x == P.req[off + n - 1].x);
+            }
         }
-        const unsigned m = __ballot_sync(KV_FULL, out);
-        if (!m) continue;
-        unsigned long long base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(P.retry_count, (unsigned long long)__popc(m));
-        base = __shfl_sync(KV_FULL, base, __ffs(m) - 1);
-        if (out) P.retry_list[base + __popc(m & ((1u << lane) - 1u))] = k;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool mine = out && (pass == 0 ? flat : !flat);
+            const unsigned m = __ballot_sync(KV_FULL, mine);
+            if (!m) continue;
+            unsigned long long *cnt = pass == 0 ? P.retry_count : other_count;
+            long long *list = pass == 0 ? P.retry_list : other;
+            unsigned long long base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+            base = __shfl_sync(KV_FULL, base, __ffs(m) - 1);
+            if (mine) list[base + __popc(m & ((1u << lane) - 1u))] = k;
+        }
     }
 }
 

@@ -637,13 +637,18 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             long long *list_b = reinterpret_cast<long long *>((char *)c->retry.p + 128);
             long long *list_a = list_b + ni;
             CUDA_TRY(c, cudaMemsetAsync(c->retry.p, 0, 64, c->stream));
+            // KVSCHED_LANE_MAXN (experiments): a lower size limit for the lane kernel, the rest
+            // going to the side stream's warp-per-instance kernel
+            if (const char *e = getenv("KVSCHED_LANE_MAXN")) P.lane_max_n = atoi(e) > 0 && atoi(e) <= LANE_NP ? atoi(e) : 0;
             {
                 KParams S = P;
                 S.retry_list = list_a;
                 S.retry_count = cnt + 1;
                 long long blocks = (inst->n_instances + 255) / 256;
                 if (blocks > 8LL * c->num_sms) blocks = 8LL * c->num_sms;
-                k_lane_split<<<(int)(blocks > 0 ? blocks : 1), 256, 0, c->stream>>>(S);
+                // out-of-scope instances: simultaneous arrivals to list A (k_mc_flatq), the
+                // rest straight to list C (k_mc_small), which the flat kernel's rejects join
+                k_lane_split<<<(int)(blocks > 0 ? blocks : 1), 256, 0, c->stream>>>(S, list_a + ni, cnt + 6);
                 CUDA_TRY(c, cudaGetLastError());
                 c->launches++;
             }
@@ -684,8 +689,15 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             long long *list_c = list_a + ni;
             const size_t key_rows = (size_t)inst->n_instances * (size_t)max_req;   // row bound
             const bool flat = key_rows * 4 <= ((size_t)2 << 30) && !grow(c, c->fkeys, key_rows * 4 + 4);
+            KParams C = A;                   // list C: k_lane_split's non-simultaneous + flat rejects
+            C.work_list = list_c;
+            C.work_count = cnt + 6;
+            C.counter = cnt + 7;
             auto fallback = [&]() -> int {
-                if (!flat) return small(A);
+                if (!flat) {
+                    const int r = small(A);
+                    return r ? r : small(C);
+                }
                 KParams F = A;
                 F.flat_keys = reinterpret_cast<uint32_t *>(c->fkeys.p);
                 F.scratch_rows = (long long)key_rows;
@@ -711,10 +723,6 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                            : launch_flatq<8>(c, k_mc_flatq<POL_MCBENCH, 8>, F, "k_mc_flatq<MCBENCH>");
 #undef KV_FLAT
                 if (r) return r;
-                KParams C = A;
-                C.work_list = list_c;
-                C.work_count = cnt + 6;
-                C.counter = cnt + 7;
                 return small(C);
             };
             if (side) {

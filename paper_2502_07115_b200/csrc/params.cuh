@@ -51,6 +51,7 @@ struct KParams {
     int2 *arr8;                 // [rows + 64] per idx (arrival order): {a, rank}
     int *capv;                  // [n_inst] round cap, -1 = instance finished by k_mc_prep / k_prot
     uint32_t *estv;             // [n_inst] work estimate (0 = nothing to simulate) or null
+    int lane_max_n;             // k_mc_lane takes instances of at most this many requests (0 = LANE_NP)
 };
 
 // Lane 0 writes the per-instance outputs.
