@@ -127,6 +127,7 @@ struct LaneFeed {
     long long base;          // first instance of the batch (warp-uniform)
     int cnt, cur;            // batch size, next instance to stage (warp-uniform)
     long long off;           // lane j: first row of instance base + j
+    long long id;            // lane j: that instance (work_list[base + j] with a work list)
     int n, M;                // lane j: its size and budget
     int4 r[LANE_NC];         // rows of instance base + cur (prefetched)
 };
@@ -156,11 +157,14 @@ __device__ __forceinline__ bool feed_claim(const KParams &P, LaneFeed &F)
     F.cnt = (int)min(32ll, P.n_inst - base);
     F.cur = 0;
     if (lane < F.cnt) {
-        const long long o0 = P.offset[base + lane];
+        const long long k = P.work_list ? P.work_list[base + lane] : base + lane;
+        const long long o0 = P.offset[k];
+        F.id = k;
         F.off = o0 - P.row_base;
-        F.n = (int)(P.offset[base + lane + 1] - o0);
-        F.M = P.mem[base + lane];
+        F.n = (int)(P.offset[k + 1] - o0);
+        F.M = P.mem[k];
     } else {
+        F.id = 0;
         F.off = 0;
         F.n = 0;
         F.M = 0;
@@ -180,7 +184,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
     while (idle) {
         const int tl = __ffs(idle) - 1;
         if (F.cur >= F.cnt && !feed_claim(P, F)) return false;
-        const long long inst = F.base + F.cur;
+        const long long inst = __shfl_sync(KV_FULL, F.id, F.cur);
         const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
         const int n = __shfl_sync(KV_FULL, F.n, F.cur);
         const int M = __shfl_sync(KV_FULL, F.M, F.cur);
