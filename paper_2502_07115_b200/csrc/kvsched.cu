@@ -674,28 +674,33 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             // profile words: bytes tau = 1 .. 4 NW with byte 4 NW - 1 never reached by a window
             const int nw = max_len < 16 ? 4 : max_len < 32 ? 8 : max_len < 52 ? 13 : 16;
             const bool sf = pol->policy == SCHED_MCSF;
-            // largest instances first: ids sorted by request count (CUB radix sort), claimed in
-            // that order, so the long instances do not end the launch.  Measured on C5: 10^6
-            // instances 2.86 -> 2.76 ms, 2.5*10^5 (a 4-GPU shard) 0.91 -> 0.81 ms, 1.25*10^5
-            // (8-GPU shard) 0.61 -> 0.49 ms; the host path's quarter-grid chunks measured slower
-            // with it (e2e 5.1 -> 5.4 ms), so it stays off there.  KVSCHED_LANE_LPT=0/1 overrides.
+            // Small batches (at most four lanes' worth of instances per lane slot: the 4- and
+            // 8-GPU shards of the strong split) claim the largest instances first -- ids sorted
+            // by request count (CUB radix sort) -- so the long instances do not end the launch:
+            // 2.5*10^5 instances 0.91 -> 0.81 ms, 1.25*10^5 0.61 -> 0.49 ms.  At 10^6 (one GPU) it
+            // gains 3 % (2.86 -> 2.76 ms) but scatters rows and results (2.56 GB of DRAM per
+            // launch instead of 1.94), so large batches keep index order; size tiers or
+            // 32-instance groups ordered by size measured no gain; the host path's quarter-grid
+            // chunks measured slower with it.  KVSCHED_LANE_LPT=0/1 overrides.
             const char *llpt = getenv("KVSCHED_LANE_LPT");
-            const bool lane_lpt = llpt ? llpt[0] == '1' : c->lane_grid_div == 1;
-            if (lane_lpt && ni > 1 && ni < (1ull << 31)) {
+            const bool lane_lpt = llpt && llpt[0] ? llpt[0] == '1'
+                                                  : c->lane_grid_div == 1 && ni <= 4ull * 32 * 16 * (size_t)c->num_sms;
+            if (lane_lpt && ni > 32 && ni < (1ull << 31)) {
+                const size_t ng = ni;
                 size_t tmp = 0;
                 cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                                          (const long long *)nullptr, (long long *)nullptr, (int)ni, 0, 32,
+                                                          (const long long *)nullptr, (long long *)nullptr, (int)ng, 0, 32,
                                                           c->stream);
-                const size_t a8 = (ni * 4 + 15) & ~(size_t)15;
-                if ((rc = grow(c, c->lpt, 2 * a8 + 2 * ni * 8 + tmp + 256))) return rc;
+                const size_t a8 = (ng * 4 + 15) & ~(size_t)15;
+                if ((rc = grow(c, c->lpt, 2 * a8 + 2 * ng * 8 + tmp + 256))) return rc;
                 char *b = reinterpret_cast<char *>(c->lpt.p);
                 uint32_t *keys = reinterpret_cast<uint32_t *>(b), *keys2 = reinterpret_cast<uint32_t *>(b + a8);
-                long long *ids = reinterpret_cast<long long *>(b + 2 * a8), *order = ids + ni;
-                k_size_keys<<<(int)std::min<long long>((long long)(ni + 255) / 256, 4LL * c->num_sms), 256, 0, c->stream>>>(
+                long long *ids = reinterpret_cast<long long *>(b + 2 * a8), *order = ids + ng;
+                k_size_keys<<<(int)std::min<long long>((long long)(ng + 255) / 256, 4LL * c->num_sms), 256, 0, c->stream>>>(
                     (long long)ni, P.offset, keys, ids);
                 CUDA_TRY(c, cudaGetLastError());
-                CUDA_TRY(c, cub::DeviceRadixSort::SortPairsDescending(b + 2 * a8 + 2 * ni * 8, tmp, keys, keys2, ids, order,
-                                                                      (int)ni, 0, 32, c->stream));
+                CUDA_TRY(c, cub::DeviceRadixSort::SortPairsDescending(b + 2 * a8 + 2 * ng * 8, tmp, keys, keys2, ids, order,
+                                                                      (int)ng, 0, 32, c->stream));
                 c->launches += 2;
                 P.work_list = order;
             }
