@@ -5,6 +5,13 @@ The product is libkvsched.so (C ABI in include/kvsched.h, CUDA kernels in csrc/)
 package holds its ctypes binding (kvsched.py), the nvcc build (build.py) and the multi-GPU
 sharding helpers (dist.py).
 """
+import os as _os
+
+# The streamed host path overlaps a persistent kernel with copy and decode work on other
+# streams; give every stream its own hardware queue (read when the CUDA context is created,
+# so this only takes effect if nothing has initialised CUDA yet; see kvsched.cu).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .kvsched import (ALPHA, ALPHA_BETA, MC_BENCH, MCSF, Context, Policy, alloc_outputs, hints_of,
                       load, simulate, to_device)
 

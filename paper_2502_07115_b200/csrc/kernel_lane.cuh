@@ -100,7 +100,7 @@ __global__ void k_lane_split(const KParams P, long long *other, unsigned long lo
             out = !lane_size_ok(P, n > 0x7fffffffll ? 0x7fffffff : (int)n, P.mem[k]);
             if (out) {
                 const long long off = P.offset[k] - P.row_base;
-                flat = !other || (n > 0 && P.req[off].x == P.req[off + n - 1].x);
+                flat = !other || (n > 0 && P.req[off].x == P.req[off + n - 1].x);   // (other = null when streaming)
             }
         }
 #pragma unroll
@@ -138,10 +138,11 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
     const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
     const int n = __shfl_sync(KV_FULL, F.n, F.cur);
     const int m = n <= LANE_NP ? n : 0;          // out-of-scope sizes are not staged
+    if (P.stream_ready && m > 0) stream_wait(P, __shfl_sync(KV_FULL, F.id, F.cur));
 #pragma unroll
     for (int c = 0; c < LANE_NC; ++c) {
         const int k = lane + 32 * c;
-        F.r[c] = k < m ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);
+        F.r[c] = k < m ? load_row(P, off + k) : make_int4(0x3fffffff, 1, 1, 1);
     }
 }
 
@@ -314,6 +315,7 @@ __device__ __forceinline__ void lane_write_result(const KParams &P, const LaneIn
     if (P.makespan) P.makespan[L.inst] = L.maxc;
     if (P.peak) P.peak[L.inst] = L.peak;
     if (P.status) P.status[L.inst] = ST_OK;
+    if (P.stream_done) stream_count(P, L.inst);
 }
 
 // max over the profile bytes, as 16x2 halves (values <= 64)

@@ -390,10 +390,11 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     }
 
     // ---- stage + validate (one coalesced 16-byte load per request) ------------------
+    stream_wait(P, inst);
     bool bad = false, slow = false;
     long long suma = 0, sumo = 0;
     for (int k = lane; k < n; k += 32) {
-        const int4 r = P.req[off + k];                   // {a, s, o, o~}
+        const int4 r = load_row(P, off + k);             // {a, s, o, o~}
         bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
         if (POL == POL_MCSF) {
             bad |= r.y + r.w > M || r.w < r.z;            // DESIGN Q8; o~ >= o

@@ -52,11 +52,52 @@ struct KParams {
     int *capv;                  // [n_inst] round cap, -1 = instance finished by k_mc_prep / k_prot
     uint32_t *estv;             // [n_inst] work estimate (0 = nothing to simulate) or null
     int lane_max_n;             // k_mc_lane takes instances of at most this many requests (0 = LANE_NP)
+    // streamed host path (sched_run_instances_host): request rows land chunk by chunk while
+    // the kernels run; instance k belongs to chunk k / stream_chunk.  A kernel waits for
+    // stream_ready[chunk] before reading an instance's rows (and reads them past L1), and
+    // counts the instance in stream_done[chunk] once its outputs are written.
+    const int *stream_ready;    // null = not streamed
+    unsigned int *stream_done;
+    int *stream_err;            // set if a wait gave up (bounded spin)
+    long long stream_chunk;
 };
+
+// wait (lane 0 spins, bounded) until the rows of instance `inst` have landed; warp-uniform
+__device__ __forceinline__ void stream_wait(const KParams &P, long long inst)
+{
+    if (!P.stream_ready) return;
+    if (lane_id() == 0) {
+        const volatile int *f = P.stream_ready + inst / P.stream_chunk;
+        long long spins = 0;
+        while (*f == 0) {
+            __nanosleep(200);
+            if (++spins > (1ll << 24)) { atomicExch(P.stream_err, 1); break; }   // ~3 s: give up
+        }
+        __threadfence();
+    }
+    __syncwarp();
+}
+
+// a request row: past L1 when rows are still landing (a cached line could predate them)
+__device__ __forceinline__ int4 load_row(const KParams &P, long long r)
+{
+    return P.stream_ready ? __ldcg(P.req + r) : P.req[r];
+}
+
+// the instance's outputs are written: count it for its chunk's release
+__device__ __forceinline__ void stream_count(const KParams &P, long long inst)
+{
+    __threadfence();
+    atomicAdd(P.stream_done + inst / P.stream_chunk, 1u);
+}
 
 // Lane 0 writes the per-instance outputs.
 __device__ __forceinline__ void write_result(const KParams &P, long long inst, const InstResult &r)
 {
+    if (P.stream_done) {                // every lane's per-request writes before the count
+        __threadfence();
+        __syncwarp();
+    }
     if (lane_id() != 0) return;
     const bool ok = r.status == ST_OK;
     if (P.tel) P.tel[inst] = ok ? r.tel : -1;
@@ -66,6 +107,7 @@ __device__ __forceinline__ void write_result(const KParams &P, long long inst, c
     if (P.makespan) P.makespan[inst] = ok ? r.makespan : -1;
     if (P.peak) P.peak[inst] = r.peak;
     if (P.status) P.status[inst] = r.status;
+    if (P.stream_done) stream_count(P, inst);
 }
 
 // Every request of an instance rejected before simulation: completion = start = -1.
