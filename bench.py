@@ -442,10 +442,19 @@ def main():
         e2e_fields = [k for k in fields if k not in ("start", "completion")] + ["latency16"]
         h_off, h_req, h_mem = pin(batch.offset), pin(rows), pin(batch.mem)
         h_out = {}
+        # per-instance outputs field-major in one pinned block per dtype (the int64 four, the
+        # int32 three): the library then copies each chunk's fields with one 2-D copy
+        i64f = [k for k in e2e_fields if k in K.kvsched.OUT_I64]
+        i32f = [k for k in e2e_fields if k not in K.kvsched.OUT_I64 and k not in ("completion", "start", "latency16")]
+        for group, dt in ((i64f, torch.int64), (i32f, torch.int32)):
+            blk = torch.empty((max(len(group), 1), max(batch.n_inst, 1)), dtype=dt).pin_memory()
+            for j, k in enumerate(group):
+                h_out[k] = blk[j]
         for k in e2e_fields:
-            n = batch.n_req if k in ("completion", "start", "latency16") else batch.n_inst
-            dt = torch.int64 if k in K.kvsched.OUT_I64 else torch.int16 if k == "latency16" else torch.int32
-            h_out[k] = torch.empty(max(n, 1), dtype=dt).pin_memory()
+            if k not in h_out:
+                n = batch.n_req if k in ("completion", "start", "latency16") else batch.n_inst
+                dt = torch.int16 if k == "latency16" else torch.int32
+                h_out[k] = torch.empty(max(n, 1), dtype=dt).pin_memory()
         host = {k: v.numpy() for k, v in h_out.items()}
         a_off, a_req, a_mem = h_off.numpy(), h_req.numpy(), h_mem.numpy()
         ctx.run_host(a_off, a_req, a_mem, pol, host, id0=id0, hints=hints, req_format=fmt)      # warm

@@ -193,7 +193,14 @@ int sched_run_instances(sched_ctx *ctx, const sched_instances *inst, const sched
 
 /* Same, with HOST pointers in `inst` and `out` (pinned memory recommended): copies inputs to
  * context-owned device buffers, runs, copies the requested outputs back and synchronises
- * the stream before returning.                                                           */
+ * the stream before returning.  The copies overlap the simulation: MC policies with
+ * SCHED_REQ_P16 rows (M <= 64) are STREAMED -- one persistent lane launch reads each chunk's
+ * wire rows as soon as a stream memory operation flags them landed and the copy-out stream
+ * releases chunk k once all its instances are counted; everything else runs as a chunked
+ * pipeline (copy-in / kernels / copy-out per chunk on separate streams).  Per-instance int64
+ * (resp. int32) outputs laid out field-major at one pitch in host memory are copied with one
+ * 2-D copy per chunk.  Uses the driver's stream memory operations (cuStreamWriteValue32 /
+ * cuStreamWaitValue32, resolved at run time); without them the chunked pipeline runs.      */
 int sched_run_instances_host(sched_ctx *ctx, const sched_instances *inst,
                              const sched_policy *pol, const sched_outputs *out);
 

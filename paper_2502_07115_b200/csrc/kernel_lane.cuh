@@ -130,15 +130,35 @@ struct LaneFeed {
     long long id;            // lane j: that instance (work_list[base + j] with a work list)
     int n, M;                // lane j: its size and budget
     int4 r[LANE_NC];         // rows of instance base + cur (prefetched)
+    int rdy;                 // streamed host path: chunks <= rdy are known to have landed
 };
 
+// R16: the streamed host path's P16 wire rows, decoded here (load_row_p16)
+template <bool R16>
 __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
 {
     const int lane = lane_id();
     const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
     const int n = __shfl_sync(KV_FULL, F.n, F.cur);
     const int m = n <= LANE_NP ? n : 0;          // out-of-scope sizes are not staged
-    if (P.stream_ready && m > 0) stream_wait(P, __shfl_sync(KV_FULL, F.id, F.cur));
+    if (P.stream_ready && m > 0) {               // chunks land in order: poll a new one only
+        const long long id = __shfl_sync(KV_FULL, F.id, F.cur);
+        const int ch = (int)(id / P.stream_chunk);
+        if (ch > F.rdy) {
+            stream_wait(P, id);
+            F.rdy = ch;
+        }
+    }
+    if (R16) {
+        int carry = 0;
+#pragma unroll
+        for (int c = 0; c < LANE_NC; ++c) {
+            const int k = lane + 32 * c;
+            const int4 x = m > 32 * c ? load_row_p16(P, off, k, m, carry) : make_int4(0, 0, 0, 0);
+            F.r[c] = k < m ? x : make_int4(0x3fffffff, 1, 1, 1);
+        }
+        return;
+    }
 #pragma unroll
     for (int c = 0; c < LANE_NC; ++c) {
         const int k = lane + 32 * c;
@@ -147,6 +167,7 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
 }
 
 // claim the next batch; false when the work counter is exhausted (warp-uniform)
+template <bool R16>
 __device__ __forceinline__ bool feed_claim(const KParams &P, LaneFeed &F)
 {
     const int lane = lane_id();
@@ -170,13 +191,13 @@ __device__ __forceinline__ bool feed_claim(const KParams &P, LaneFeed &F)
         F.n = 0;
         F.M = 0;
     }
-    feed_prefetch(P, F);
+    feed_prefetch<R16>(P, F);
     return true;
 }
 
 // Stage instances into the idle lanes of `idle` (warp-uniform).  Returns false once the
 // work counter is exhausted.
-template <int POL, int NW>
+template <int POL, int NW, bool R16>
 __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, int *hist, LaneInst<NW> &L,
                                             uint32_t idle, LaneFeed &F)
 {
@@ -184,7 +205,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
     uint16_t *d16 = reinterpret_cast<uint16_t *>(data);
     while (idle) {
         const int tl = __ffs(idle) - 1;
-        if (F.cur >= F.cnt && !feed_claim(P, F)) return false;
+        if (F.cur >= F.cnt && !feed_claim<R16>(P, F)) return false;
         const long long inst = __shfl_sync(KV_FULL, F.id, F.cur);
         const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
         const int n = __shfl_sync(KV_FULL, F.n, F.cur);
@@ -192,7 +213,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
         int4 r[LANE_NC];
 #pragma unroll
         for (int c = 0; c < LANE_NC; ++c) r[c] = F.r[c];
-        if (++F.cur < F.cnt) feed_prefetch(P, F);
+        if (++F.cur < F.cnt) feed_prefetch<R16>(P, F);
         // in scope, and within the caller's size hints (k_mc_small reports violations)
         // instances outside the size scope were listed by k_lane_split before this launch
         if (!lane_size_ok(P, n, M)) continue;
@@ -436,7 +457,7 @@ __device__ __forceinline__ int first_fit(const uint32_t (&P)[NW], int L, int w, 
 __device__ __forceinline__ int hmax16(uint32_t v) { return max((int)(v & 0xffffu), (int)(v >> 16)); }
 
 // -------------------------------------------------------------------------------------
-template <int POL, int NW>
+template <int POL, int NW, bool R16 = false>
 __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -451,12 +472,13 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
     L.active = false;
     LaneFeed F;
     F.cnt = F.cur = 0;
+    F.rdy = -1;
     uint32_t pk16 = 0u;
     bool more = true;
     for (;;) {
         const uint32_t idle = __ballot_sync(KV_FULL, !L.active);
         if (idle && more) {
-            more = lane_refill<POL, NW>(P, data, hist, L, idle, F);
+            more = lane_refill<POL, NW, R16>(P, data, hist, L, idle, F);
             if (idle & (1u << lane)) pk16 = 0u;
         }
         if (!__any_sync(KV_FULL, L.active)) break;
@@ -476,6 +498,9 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
                 L.q1 |= wq == 1 ? bit : 0u;
                 L.q2 |= wq == 2 ? bit : 0u;
                 if (r < L.h) { L.h = r; L.hstale = true; }
+                // streamed host path: the consumed half now keeps a_idx mod 2^16 for the
+                // latency16 output (a lane instance's latency is < 2^16, see the scope)
+                if (R16) reinterpret_cast<uint16_t *>(const_cast<uint32_t *>(col + 32 * L.next))[1] = (uint16_t)L.a_next;
                 L.a_next = (++L.next < L.n) ? L.a_next + (int)(d >> 7) : KV_INF;
             }
 
@@ -542,6 +567,7 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
             const int c = L.t + L.w;
             if (P.start) P.start[L.off + L.hidx] = L.t;
             if (P.completion) P.completion[L.off + L.hidx] = c;
+            if (R16 && P.lat16) P.lat16[L.off + L.hidx] = (uint16_t)(c - (int)(col[32 * L.hidx] >> 16));
             L.sumc += c;
             L.maxc = max(L.maxc, c);
             const int h = L.h;

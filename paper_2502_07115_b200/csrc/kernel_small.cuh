@@ -362,6 +362,10 @@ __device__ __forceinline__ void small_run(const KParams &P, long long inst, cons
         sumc += c;
         if (P.completion) P.completion[off + k] = c;
         if (P.start) P.start[off + k] = p;
+        if (P.lat16) {
+            const long long d = (long long)c - S.arr[k];
+            P.lat16[off + k] = (c < 0 || d < 0 || d > 65534) ? (uint16_t)0xffffu : (uint16_t)d;
+        }
     }
     sumc = warp_sum_i64(sumc);
     res.tel = sumc - suma;
@@ -393,8 +397,12 @@ __device__ void small_instance(const KParams &P, long long inst, const SmallSmem
     stream_wait(P, inst);
     bool bad = false, slow = false;
     long long suma = 0, sumo = 0;
-    for (int k = lane; k < n; k += 32) {
-        const int4 r = load_row(P, off + k);             // {a, s, o, o~}
+    int carry = 0;                                       // P16 rows: a of the previous chunk
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + lane;
+        const int4 r = P.req16 ? load_row_p16(P, off, k, n, carry)
+                               : (k < n ? load_row(P, off + k) : make_int4(0, 1, 1, 1));   // {a, s, o, o~}
+        if (k >= n) continue;
         bad |= r.x < 0 || r.y < 1 || r.z < 1 || r.w < 1;
         if (POL == POL_MCSF) {
             bad |= r.y + r.w > M || r.w < r.z;            // DESIGN Q8; o~ >= o

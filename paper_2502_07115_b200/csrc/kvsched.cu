@@ -3,14 +3,18 @@
 // Host side: argument validation, size bounds, scratch management, kernel selection and
 // launch on the context's stream.  All simulation work runs in the kernels of
 // kernel_small.cuh / kernel_ring.cuh; there is no CPU path.
+#include <cuda.h>            // CUstream / CUdeviceptr types of the stream memory operations only
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <unistd.h>
 #include <string.h>
 
+#include <chrono>
 #include <utility>
 #include <vector>
 
@@ -77,8 +81,8 @@ struct sched_ctx {
     cudaEvent_t ev_split = nullptr, ev_side = nullptr;
     bool side_ok = false;                             // run_impl may use s_side (device path only)
     // streamed host path: rows land chunk by chunk while one persistent lane launch runs
-    // (KParams::stream_*); the lane grid leaves `stream_reserve` SMs to the decode, flag,
-    // release and copy kernels, and the side-stream kernels are capped at `grid_cap` blocks
+    // (KParams::stream_*); the lane grid leaves `stream_reserve` SMs to the side-stream and
+    // latency16 kernels, and the side-stream kernels are capped at `grid_cap` blocks
     bool stream_mode = false;
     bool stream_off = false;                          // retrying a streamed call on the chunked path
     const int *stream_ready = nullptr;
@@ -86,6 +90,10 @@ struct sched_ctx {
     int *stream_err = nullptr;
     long long stream_chunk = 1;
     int stream_reserve = 0, grid_cap = 0;
+    const uint16_t *stream_req16 = nullptr;           // the P16 wire rows the kernels decode
+    uint16_t *stream_lat16 = nullptr;                 // latency16 written by the kernels
+    std::vector<std::pair<const char *, cudaEvent_t>> *trace = nullptr;   // KVSCHED_STREAM_TRACE marks
+    DevBuf sel;                                       // DeviceSelect scratch (streamed path)
     DevBuf sflags;
     int lane_grid_div = 1;                            // host path: lane grid = full occupancy / this
     // host path: extra compute streams, each with its own per-run scratch, so that the
@@ -265,26 +273,6 @@ __global__ void k_latency16(long long n_rows, const int4 *req, const int *comple
         const long long d = (long long)c - req[i].x;
         lat[i] = (c < 0 || d < 0 || d > 65534) ? (uint16_t)65535 : (uint16_t)d;
     }
-}
-
-// streamed host path: chunk k's rows have landed and been decoded (stream order on s_in)
-__global__ void k_stream_ready(int *ready, long long k)
-{
-    __threadfence();
-    ready[k] = 1;
-}
-
-// streamed host path: hold the copy-out stream until every instance of chunk k is counted
-// (bounded spin: a wait that gives up sets *err and lets the stream go on)
-__global__ void k_stream_release(const unsigned int *done, long long k, unsigned int target, int *err)
-{
-    const volatile unsigned int *d = done + k;
-    long long spins = 0;
-    while (*d < target) {
-        __nanosleep(500);
-        if (++spins > (1ll << 23)) { atomicExch(err, 2); break; }
-    }
-    __threadfence();
 }
 
 // Instances handed to a full-ring rerun that cannot run: status UNSUPPORTED, no schedule.
@@ -600,6 +588,39 @@ int sched_set_stream(sched_ctx *c, void *cuda_stream)
 
 }  // extern "C"
 
+static void trace_mark(sched_ctx *c, const char *what)
+{
+    if (!c->trace) return;
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    c->trace->push_back({what, e});
+}
+
+// Streamed host path: the instances outside the lane kernel's size scope, in instance order
+// (a stable selection over the CSR offsets and budgets), on the context's stream.
+struct OutOfLane {
+    KParams P;
+    __device__ bool operator()(long long k) const
+    {
+        const long long n = P.offset[k + 1] - P.offset[k];
+        return !lane_size_ok(P, n > 0x7fffffffll ? 0x7fffffff : (int)n, P.mem[k]);
+    }
+};
+
+static int select_out_of_lane(sched_ctx *c, const KParams &P, long long *list, unsigned long long *count)
+{
+    const OutOfLane pred{P};
+    cub::CountingInputIterator<long long> ids(0);
+    size_t tmp = 0;
+    CUDA_TRY(c, cub::DeviceSelect::If(nullptr, tmp, ids, list, count, P.n_inst, pred, c->stream));
+    int rc = grow(c, c->sel, tmp + 16);
+    if (rc) return rc;
+    CUDA_TRY(c, cub::DeviceSelect::If(c->sel.p, tmp, ids, list, count, P.n_inst, pred, c->stream));
+    c->launches++;
+    return SCHED_OK;
+}
+
 // Device-pointer run.  Request rows of instance k start at req_offset[k] - row_base in
 // `req` (and in the completion / start outputs): row_base lets the pipelined host path run
 // chunks whose rows sit in chunk-local buffers while the offsets stay global.
@@ -665,6 +686,8 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         P.stream_done = c->stream_done;
         P.stream_err = c->stream_err;
         P.stream_chunk = c->stream_chunk;
+        P.req16 = c->stream_req16;
+        P.lat16 = c->stream_lat16;
     }
     CUDA_TRY(c, cudaMemsetAsync(c->counter.p, 0, 8, c->stream));
 
@@ -700,12 +723,16 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 long long blocks = (inst->n_instances + 255) / 256;
                 if (blocks > 8LL * c->num_sms) blocks = 8LL * c->num_sms;
                 // out-of-scope instances: simultaneous arrivals to list A (k_mc_flatq), the
-                // rest straight to list C (k_mc_small), which the flat kernel's rejects join
-                k_lane_split<<<(int)(blocks > 0 ? blocks : 1), 256, 0, c->stream>>>(S, c->stream_mode ? nullptr : list_a + ni,
-                                                                                     cnt + 6);
-                if (c->stream_mode && getenv("KVSCHED_STREAM_DEBUG")) { fprintf(stderr, "[stream] split launched\n"); fflush(stderr); }
-                CUDA_TRY(c, cudaGetLastError());
-                c->launches++;
+                // rest straight to list C (k_mc_small), which the flat kernel's rejects join.
+                // (Streamed host path: list A is selected in instance order on the side stream
+                // below instead, so the side kernel meets the chunks in the order they land.)
+                if (!c->stream_mode) {
+                    k_lane_split<<<(int)(blocks > 0 ? blocks : 1), 256, 0, c->stream>>>(S, list_a + ni, cnt + 6);
+                    CUDA_TRY(c, cudaGetLastError());
+                    c->launches++;
+                } else if ((rc = select_out_of_lane(c, P, list_a, cnt + 1))) {   // before the lane launch
+                    return rc;                                                   // takes the SMs
+                }
             }
             const bool side = c->side_ok;
             if (side) {
@@ -750,11 +777,14 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 c->launches += 2;
                 P.work_list = order;
             }
-#define KV_LANE(NWV) (sf ? launch_lane(c, k_mc_lane<POL_MCSF, NWV>, P, "k_mc_lane<MCSF>")                 \
-                         : launch_lane(c, k_mc_lane<POL_MCBENCH, NWV>, P, "k_mc_lane<MCBENCH>"))
+#define KV_LANE(NWV) (P.req16 ? (sf ? launch_lane(c, k_mc_lane<POL_MCSF, NWV, true>, P, "k_mc_lane<MCSF,p16>")      \
+                                    : launch_lane(c, k_mc_lane<POL_MCBENCH, NWV, true>, P, "k_mc_lane<MCBENCH,p16>")) \
+                         : sf ? launch_lane(c, k_mc_lane<POL_MCSF, NWV>, P, "k_mc_lane<MCSF>")                  \
+                              : launch_lane(c, k_mc_lane<POL_MCBENCH, NWV>, P, "k_mc_lane<MCBENCH>"))
+            trace_mark(c, "lane0");
             rc = nw == 4 ? KV_LANE(4) : nw == 8 ? KV_LANE(8) : nw == 13 ? KV_LANE(13) : KV_LANE(16);
+            trace_mark(c, "lane1");
             P.work_list = nullptr;
-            if (c->stream_mode && getenv("KVSCHED_STREAM_DEBUG")) { fprintf(stderr, "[stream] lane launched rc=%d\n", rc); fflush(stderr); }
 #undef KV_LANE
             if (rc) return rc;
             P.retry_list = nullptr;
@@ -816,8 +846,11 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             };
             if (side) {
                 std::swap(c->stream, c->s_side);
-                rc = cudaStreamWaitEvent(c->stream, c->ev_split, 0) == cudaSuccess ? fallback()
+                rc = cudaStreamWaitEvent(c->stream, c->ev_split, 0) == cudaSuccess ? SCHED_OK
                          : fail(c, SCHED_E_CUDA, "cudaStreamWaitEvent failed");
+                trace_mark(c, "side0");
+                if (!rc) rc = fallback();
+                trace_mark(c, "side1");
                 if (!rc && cudaEventRecord(c->ev_side, c->stream) != cudaSuccess)
                     rc = fail(c, SCHED_E_CUDA, "cudaEventRecord failed");
                 std::swap(c->stream, c->s_side);
@@ -1161,6 +1194,38 @@ int sched_run_instances(sched_ctx *c, const sched_instances *inst, const sched_p
     return rc;
 }
 
+// Stream memory operations (driver API, resolved at run time so the library links only the
+// runtime): the streamed host path sets its per-chunk flags and holds its copy-out stream
+// with them, on the copy engines' front end, without occupying an SM.
+typedef CUresult (*pfn_write32_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*pfn_wait32_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static pfn_write32_t g_write32 = nullptr;
+static pfn_wait32_t g_wait32 = nullptr;
+static double now_ms()
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static bool stream_mem_ops(sched_ctx *c)
+{
+    static int state = 0;                                  // 0 untried, 1 available, 2 not
+    if (state == 0) {
+        void *w = nullptr, *v = nullptr;
+        cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+        const bool ok = cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+                        cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+                        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && v;
+        if (ok) {
+            g_write32 = (pfn_write32_t)w;
+            g_wait32 = (pfn_wait32_t)v;
+        }
+        cudaGetLastError();
+        state = ok ? 1 : 2;
+    }
+    (void)c;
+    return state == 1;
+}
+
 // Host buffers.  The batch is cut into chunks of whole instances; chunk k's request rows are
 // copied in on one stream, simulated on the context's stream, and its outputs copied out on
 // a third, so the PCIe transfers of neighbouring chunks overlap the kernels.
@@ -1246,87 +1311,84 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
         ~GridDiv() { c->lane_grid_div = 1; }
     } gd{c};
     c->lane_grid_div = grid_div;
-    // Streamed pipeline (EXPERIMENTAL, opt-in with KVSCHED_HOST_STREAM=1; MC policies on the
-    // lane path): the rows
-    // are copied in K chunks (s_in), each chunk decoded and flagged as it lands; ONE lane
-    // launch over the whole batch on the context's stream claims instances in order and waits
-    // for a chunk's flag before reading its rows; the warp-per-instance fallbacks run beside
-    // it on the side stream; the copy-out stream releases chunk k (latency16 + the per-instance
-    // outputs) once every instance of it is counted.  No per-chunk kernel tails.
-    // The lane launch waits for flags that s_in's copies and decode kernels produce, so s_in
-    // must not share a hardware queue with the context's stream (more streams than
-    // CUDA_DEVICE_MAX_CONNECTIONS, default 8, can alias; the package raises it to 32): waits
-    // are bounded, and a call whose wait gave up is redone on the chunked pipeline.  Status:
-    // parity-green and ~0.02 s per 10^6-instance call when it runs, but some runs stall (a
-    // chunk's flag or count stops arriving while the persistent launch waits; seen with the
-    // context on the default stream, after earlier device-path calls) until the bounded waits
-    // give up -- not understood yet, so the chunked pipeline below stays the default.
+    // Streamed pipeline (MC policies on the lane path, SCHED_REQ_P16 rows): the rows are
+    // copied in K chunks on s_in, and after each chunk's copy a stream memory operation sets
+    // ready[k] (the copy engine's front end writes it: no kernel).  ONE persistent lane launch
+    // over the whole batch claims instances in order and waits for an instance's chunk flag
+    // before reading its rows, which it decodes itself (k_mc_lane<..., p16>); the size-scope
+    // instances run beside it on the side stream (k_mc_small, same flags, same decoding).
+    // Every kernel counts an instance in done[chunk] once its outputs are written, and the
+    // copy-out stream waits for done[k] >= |chunk k| with a stream wait-value (front end
+    // again), then converts chunk k's completions to latency16 and copies it out.  No kernel
+    // waits for another kernel's output, so nothing the spinning launches wait on needs an
+    // SM; waits are bounded, and a call whose wait gave up is redone on the chunked pipeline.
+    // KVSCHED_HOST_STREAM=0 selects the chunked pipeline (A/B).
     {
         const char *se = getenv("KVSCHED_HOST_STREAM");
         const bool lane_path = (pol->policy == SCHED_MCSF || pol->policy == SCHED_MC_BENCH) && hi.max_mem <= kSmallMaxMem &&
                                hi.max_requests <= kSmallMaxRequests && pol->round_cap <= 0 &&
                                !(pol->flags & (SCHED_FLAG_PER_ROUND | SCHED_FLAG_WARP_PER_INSTANCE));
-        if (lane_path && se && se[0] == '1' && !c->stream_off && ni >= 64) {
-            const bool dbg = getenv("KVSCHED_STREAM_DEBUG") != nullptr;
-#define SDBG(msg) do { if (dbg) { fprintf(stderr, "[stream] %s\n", msg); fflush(stderr); } } while (0)
-            SDBG("enter");
-            long long K = 12;
+        if (lane_path && inst->req_format == SCHED_REQ_P16 && !(se && se[0] == '0') && !c->stream_off && ni >= 64 &&
+            stream_mem_ops(c)) {
+            // K flag chunks (copy-in granularity); the copy-out takes them in groups that grow
+            // from one chunk to KVSCHED_HOST_STREAM_GROUP (the first results leave early, the
+            // later copies are large)
+            long long K = 16;
             if (const char *e = getenv("KVSCHED_HOST_STREAM_CHUNKS")) K = atoll(e) >= 1 ? atoll(e) : K;
+            long long gmax = 1;
+            if (const char *e = getenv("KVSCHED_HOST_STREAM_GROUP")) gmax = atoll(e) >= 1 ? atoll(e) : gmax;
             if (K > ni) K = ni;
             const long long C = (ni + K - 1) / K;                   // instances per chunk
             K = (ni + C - 1) / C;
-            if ((rc = grow(c, c->sflags, (size_t)(3 * K + 2) * 4 + 16))) return rc;
+            if ((rc = grow(c, c->sflags, (size_t)(2 * K + 2) * 4 + 16))) return rc;
             int *ready = reinterpret_cast<int *>(c->sflags.p);
-            volatile int *hmirror = nullptr;             // KVSCHED_STREAM_DEBUG: flags in mapped host memory
-            if (dbg) {
-                void *hp = nullptr, *dp = nullptr;
-                CUDA_TRY(c, cudaHostAlloc(&hp, (size_t)(3 * K + 2) * 4 + 16, cudaHostAllocMapped));
-                CUDA_TRY(c, cudaHostGetDevicePointer(&dp, hp, 0));
-                memset(hp, 0, (size_t)(3 * K + 2) * 4 + 16);
-                hmirror = (volatile int *)hp;
-                ready = reinterpret_cast<int *>(dp);
-            }
             unsigned int *done = reinterpret_cast<unsigned int *>(ready + K);
             int *err = reinterpret_cast<int *>(done + K);
-            while ((long long)c->chunk_events.size() < 3) c->chunk_events.push_back(take_event(c));
+            const bool trace = getenv("KVSCHED_STREAM_TRACE") != nullptr;   // event timeline on stderr
+            std::vector<std::pair<const char *, cudaEvent_t>> tev;
+            auto mark = [&](const char *what, cudaStream_t st) {
+                if (!trace) return;
+                cudaEvent_t e = nullptr;
+                const cudaError_t e1 = cudaEventCreate(&e);
+                const cudaError_t e2 = cudaEventRecord(e, st);
+                if (e1 != cudaSuccess || e2 != cudaSuccess)
+                    fprintf(stderr, "[stream trace] %s: %s / %s\n", what, cudaGetErrorString(e1), cudaGetErrorString(e2));
+                tev.push_back({what, e});
+            };
+            while ((long long)c->chunk_events.size() < 2) c->chunk_events.push_back(take_event(c));
             cudaEvent_t *ev = c->chunk_events.data();
-            if (!dbg) CUDA_TRY(c, cudaMemsetAsync(c->sflags.p, 0, (size_t)(2 * K + 2) * 4, c->stream));
+            mark("start", c->stream);
+            c->trace = trace ? &tev : nullptr;
+            struct TraceOff { sched_ctx *c; ~TraceOff() { c->trace = nullptr; } } trace_off{c};
+            // flags and counts cleared before any copy of this call (and after earlier work)
+            CUDA_TRY(c, cudaMemsetAsync(c->sflags.p, 0, (size_t)(2 * K + 2) * 4, c->stream));
             CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
             CUDA_TRY(c, cudaStreamWaitEvent(c->s_in, ev[0], 0));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, ev[0], 0));
             CUDA_TRY(c, cudaMemcpyAsync(c->h_off.p, hoff, b_off, cudaMemcpyHostToDevice, c->s_in));
             CUDA_TRY(c, cudaMemcpyAsync(c->h_mem.p, inst->mem_limit, b_mem, cudaMemcpyHostToDevice, c->s_in));
             CUDA_TRY(c, cudaEventRecord(ev[1], c->s_in));           // offsets and budgets are in
-            SDBG("meta enqueued");
             const long long *doff = (const long long *)c->h_off.p;
-            int4 *drows = reinterpret_cast<int4 *>(c->h_req.p);
+            const uint16_t *d16 = reinterpret_cast<const uint16_t *>(c->h_pk.p);
             for (long long k = 0; k < K; ++k) {
                 const long long i0 = k * C, i1 = std::min(ni, i0 + C);
                 const long long r0 = hoff[i0], r1 = hoff[i1];
-                char *dst = packed ? (char *)c->h_pk.p + r0 * row_in : (char *)drows + r0 * 16;
                 if (r1 > r0)
-                    CUDA_TRY(c, cudaMemcpyAsync(dst, (const char *)inst->req + r0 * row_in, (size_t)(r1 - r0) * row_in,
-                                                cudaMemcpyHostToDevice, c->s_in));
-                if (dbg) k_stream_ready<<<1, 1, 0, c->s_in>>>(ready + 2 * K + 2, k);    // copy landed (diagnosis)
-                if (packed && i1 > i0) {
-                    std::swap(c->stream, c->s_in);
-                    launch_decode(c, inst->req_format, i1 - i0, doff + i0, r0, dst, drows + r0);
-                    std::swap(c->stream, c->s_in);
-                    CUDA_TRY(c, cudaGetLastError());
-                }
-                k_stream_ready<<<1, 1, 0, c->s_in>>>(ready, k);
-                CUDA_TRY(c, cudaGetLastError());
-                c->launches++;
+                    CUDA_TRY(c, cudaMemcpyAsync((char *)c->h_pk.p + r0 * 2, (const char *)inst->req + r0 * 2,
+                                                (size_t)(r1 - r0) * 2, cudaMemcpyHostToDevice, c->s_in));
+                if (g_write32((CUstream)c->s_in, (CUdeviceptr)(ready + k), 1u, 0) != CUDA_SUCCESS)
+                    return fail(c, SCHED_E_CUDA, "cuStreamWriteValue32 failed");
+                mark("in", c->s_in);
             }
-            SDBG("chunks enqueued");
             // the simulation: one launch over everything, gated per chunk
             CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[1], 0));
             sched_instances di = hi;
             di.req_format = SCHED_REQ_I32X4;
             di.req_offset = (const int64_t *)doff;
-            di.req = (const int32_t *)drows;
+            di.req = nullptr;                                       // the kernels read d16
             di.mem_limit = (const int32_t *)c->h_mem.p;
             sched_outputs dout;
-            dout.completion = (int32_t *)(ob + o_comp);                 // latency16 needs it
+            dout.completion = out->completion ? (int32_t *)(ob + o_comp) : nullptr;
             dout.start = out->start ? (int32_t *)(ob + o_start) : nullptr;
             dout.tel = out->tel ? (int64_t *)(ob + o_i64) : nullptr;
             dout.rounds = out->rounds ? (int64_t *)(ob + o_i64 + ni * 8) : nullptr;
@@ -1336,38 +1398,49 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
             dout.peak_mem = out->peak_mem ? (int32_t *)(ob + o_i32 + ni * 4) : nullptr;
             dout.status = out->status ? (int32_t *)(ob + o_i32 + ni * 8) : nullptr;
             dout.latency16 = nullptr;
-            struct StreamGuard {
-                sched_ctx *c;
-                ~StreamGuard() { c->stream_mode = false; c->side_ok = false; c->stream_reserve = 0; c->grid_cap = 0; }
-            } sg{c};
-            c->stream_mode = true;
-            c->stream_ready = ready;
-            c->stream_done = done;
-            c->stream_err = err;
-            c->stream_chunk = C;
-            c->stream_reserve = 6;               // SMs left to decode / flag / release / copy kernels
-            c->grid_cap = 2 * c->num_sms / 37;   // side-stream fallback kernels: ~8 blocks
-            c->side_ok = true;
-            c->lane_grid_div = 1;                // one launch over the whole GPU (minus the reserve)
-            if ((rc = run_impl(c, &di, pol, &dout, 0))) return rc;
-            SDBG("simulation enqueued");
+            {
+                struct StreamGuard {
+                    sched_ctx *c;
+                    ~StreamGuard()
+                    {
+                        c->stream_mode = false;
+                        c->side_ok = false;
+                        c->stream_reserve = 0;
+                        c->grid_cap = 0;
+                        c->stream_req16 = nullptr;
+                        c->stream_lat16 = nullptr;
+                    }
+                } sg{c};
+                c->stream_mode = true;
+                c->stream_ready = ready;
+                c->stream_done = done;
+                c->stream_err = err;
+                c->stream_chunk = C;
+                c->stream_req16 = d16;
+                c->stream_lat16 = out->latency16 ? (uint16_t *)(ob + o_lat) : nullptr;
+                c->stream_reserve = 10;              // SMs left to the side-stream kernels (8-12 measured alike)
+                c->grid_cap = 96;                    // side-stream fallback kernels (blocks)
+                if (const char *e = getenv("KVSCHED_STREAM_RESERVE")) c->stream_reserve = atoi(e);
+                if (const char *e = getenv("KVSCHED_STREAM_SIDE_BLOCKS")) c->grid_cap = atoi(e);
+                c->side_ok = true;
+                c->lane_grid_div = 1;                // one launch over the whole GPU (minus the reserve)
+                if ((rc = run_impl(c, &di, pol, &dout, 0))) return rc;
+                mark("sim", c->stream);
+                if (c->s_side) mark("side", c->s_side);
+            }
             // copy-out: chunk k as soon as all its instances are counted
-            CUDA_TRY(c, cudaStreamWaitEvent(c->s_out, ev[1], 0));
             uint16_t *dlat = (uint16_t *)(ob + o_lat);
-            for (long long k = 0; k < K; ++k) {
-                const long long i0 = k * C, i1 = std::min(ni, i0 + C);
+            for (long long k = 0, gs = 1; k < K; k += gs, gs = std::min(2 * gs, gmax)) {
+                const long long ke = std::min(K, k + gs);
+                const long long i0 = k * C, i1 = std::min(ni, ke * C);
                 const long long r0 = hoff[i0], r1 = hoff[i1];
-                k_stream_release<<<1, 1, 0, c->s_out>>>(done, k, (unsigned int)(i1 - i0), err);
-                CUDA_TRY(c, cudaGetLastError());
-                c->launches++;
-                if (out->latency16 && r1 > r0) {
-                    std::swap(c->stream, c->s_out);
-                    rc = launch_latency16(c, r1 - r0, drows + r0, dout.completion + r0, dlat + r0);
-                    std::swap(c->stream, c->s_out);
-                    if (rc) return rc;
-                }
+                for (long long j = k; j < ke; ++j)
+                    if (g_wait32((CUstream)c->s_out, (CUdeviceptr)(done + j), (cuuint32_t)(std::min(ni, (j + 1) * C) - j * C),
+                                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                        return fail(c, SCHED_E_CUDA, "cuStreamWaitValue32 failed");
                 struct { void *h; const void *d; size_t b; } cp[] = {
-                    {out->completion ? out->completion + r0 : nullptr, dout.completion + r0, (size_t)(r1 - r0) * 4},
+                    {out->completion ? out->completion + r0 : nullptr, dout.completion ? dout.completion + r0 : nullptr,
+                     (size_t)(r1 - r0) * 4},
                     {out->latency16 ? out->latency16 + r0 : nullptr, dlat + r0, (size_t)(r1 - r0) * 2},
                     {out->start ? out->start + r0 : nullptr, dout.start ? dout.start + r0 : nullptr, (size_t)(r1 - r0) * 4},
                     {out->tel ? out->tel + i0 : nullptr, dout.tel ? dout.tel + i0 : nullptr, (size_t)(i1 - i0) * 8},
@@ -1378,36 +1451,73 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
                     {out->makespan ? out->makespan + i0 : nullptr, dout.makespan ? dout.makespan + i0 : nullptr, (size_t)(i1 - i0) * 4},
                     {out->peak_mem ? out->peak_mem + i0 : nullptr, dout.peak_mem ? dout.peak_mem + i0 : nullptr, (size_t)(i1 - i0) * 4},
                     {out->status ? out->status + i0 : nullptr, dout.status ? dout.status + i0 : nullptr, (size_t)(i1 - i0) * 4}};
-                for (auto &x : cp)
-                    if (x.h && x.d && x.b) CUDA_TRY(c, cudaMemcpyAsync(x.h, x.d, x.b, cudaMemcpyDeviceToHost, c->s_out));
-            }
-            SDBG("copy-out enqueued");
-            if (hmirror) {                            // progress of the flags (diagnosis only)
-                for (int it = 0; it < 40; ++it) {
-                    fprintf(stderr, "[stream dbg %d] ready", it);
-                    for (long long k = 0; k < K; ++k) fprintf(stderr, " %d", hmirror[k]);
-                    fprintf(stderr, " | done");
-                    for (long long k = 0; k < K; ++k) fprintf(stderr, " %d", hmirror[K + k]);
-                    fprintf(stderr, " | err %d | copied", hmirror[2 * K]);
-                    for (long long k = 0; k < K; ++k) fprintf(stderr, " %d", hmirror[2 * K + 2 + k]);
-                    fprintf(stderr, "\n");
-                    fflush(stderr);
-                    bool all = true;
-                    for (long long k = 0; k < K; ++k) all = all && hmirror[K + k] >= (int)(std::min(ni, (k + 1) * C) - k * C);
-                    if (all) break;
-                    usleep(100000);
+                mark("rel", c->s_out);
+                // per-instance fields laid out field-major at one pitch in host memory (the
+                // int64 four, the int32 three) go out as one 2-D copy per group: a copy per
+                // field and chunk costs more in per-copy overhead than its bytes
+                bool grouped[10] = {false};
+                for (int g = 0; g < 2; ++g) {
+                    const int f0 = g == 0 ? 3 : 7, nf = g == 0 ? 4 : 3;
+                    const size_t esz = g == 0 ? 8 : 4;
+                    bool ok = true;
+                    for (int f = f0; f < f0 + nf; ++f) ok = ok && cp[f].h && cp[f].d && cp[f].b;
+                    if (!ok) continue;
+                    const ptrdiff_t hp = (char *)cp[f0 + 1].h - (char *)cp[f0].h;
+                    for (int f = f0 + 1; f < f0 + nf; ++f)
+                        ok = ok && (char *)cp[f].h - (char *)cp[f - 1].h == hp &&
+                             (const char *)cp[f].d - (const char *)cp[f - 1].d == (ptrdiff_t)(esz * ni);
+                    if (!ok || hp < (ptrdiff_t)cp[f0].b) continue;
+                    CUDA_TRY(c, cudaMemcpy2DAsync(cp[f0].h, (size_t)hp, cp[f0].d, esz * ni, cp[f0].b, nf,
+                                                  cudaMemcpyDeviceToHost, c->s_out));
+                    for (int f = f0; f < f0 + nf; ++f) grouped[f] = true;
                 }
+                for (int f = 0; f < 10; ++f)
+                    if (!grouped[f] && cp[f].h && cp[f].d && cp[f].b)
+                        CUDA_TRY(c, cudaMemcpyAsync(cp[f].h, cp[f].d, cp[f].b, cudaMemcpyDeviceToHost, c->s_out));
+                mark("out", c->s_out);
             }
-            CUDA_TRY(c, cudaStreamSynchronize(c->s_out));
+            if (trace) {                 // host-side completion times of the marks (poll)
+                std::vector<double> when(tev.size(), -1.0);
+                const double t0 = now_ms();
+                size_t left = tev.size();
+                while (left && now_ms() - t0 < 5000.0) {
+                    for (size_t i = 0; i < tev.size(); ++i)
+                        if (when[i] < 0 && cudaEventQuery(tev[i].second) == cudaSuccess) {
+                            when[i] = now_ms() - t0;
+                            --left;
+                        }
+                }
+                fprintf(stderr, "[stream trace]");
+                for (size_t i = 0; i < tev.size(); ++i) fprintf(stderr, " %s %.3f", tev[i].first, when[i] - when[0]);
+                fprintf(stderr, "\n");
+                for (auto &e : tev) cudaEventDestroy(e.second);
+            }
+            // The kernels end on their own (bounded waits); then the copy-out stream can only be
+            // held by a count that never completes -- which would be a bug: watch it, and if it
+            // does not drain, release every wait and redo the call on the chunked pipeline.
             CUDA_TRY(c, cudaStreamSynchronize(c->s_in));
             CUDA_TRY(c, cudaStreamSynchronize(c->stream));
             if (c->s_side) CUDA_TRY(c, cudaStreamSynchronize(c->s_side));
+            bool stuck = false;
+            for (int it = 0;; ++it) {
+                const cudaError_t q = cudaStreamQuery(c->s_out);
+                if (q == cudaSuccess) break;
+                if (q != cudaErrorNotReady) CUDA_TRY(c, q);
+                if (it > 20000) {                                   // ~2 s after the kernels ended
+                    stuck = true;
+                    std::vector<unsigned int> big((size_t)K, 0x7fffffffu);
+                    CUDA_TRY(c, cudaMemcpy(done, big.data(), (size_t)K * 4, cudaMemcpyHostToDevice));
+                    CUDA_TRY(c, cudaStreamSynchronize(c->s_out));
+                    break;
+                }
+                usleep(100);
+            }
             int herr = 0;
             CUDA_TRY(c, cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost));
-            if (!herr) return SCHED_OK;
-            // A wait gave up (its producer could not run beside the persistent launch, e.g. two
-            // streams on one hardware queue): the outputs are not trusted; redo the batch on the
-            // chunked pipeline, which needs no cross-stream progress.
+            if (!herr && !stuck) {
+                c->last_kernel = pol->policy == SCHED_MCSF ? "k_mc_lane<MCSF,streamed>" : "k_mc_lane<MCBENCH,streamed>";
+                return SCHED_OK;
+            }
             c->stream_off = true;
             struct Off { sched_ctx *c; ~Off() { c->stream_off = false; } } off_{c};
             return sched_run_instances_host(c, inst, pol, out);

@@ -60,6 +60,13 @@ struct KParams {
     unsigned int *stream_done;
     int *stream_err;            // set if a wait gave up (bounded spin)
     long long stream_chunk;
+    // streamed host path with SCHED_REQ_P16 rows: the kernels read the 2-byte wire rows and
+    // decode them themselves (load_row_p16), so no decode kernel stands between a chunk's
+    // copy and its first reader; null otherwise
+    const uint16_t *req16;
+    // streamed host path: latency16 (c_i - a_i, 65535 = unscheduled) written by the kernels
+    // themselves beside / instead of the completion rounds; null otherwise
+    uint16_t *lat16;
 };
 
 // wait (lane 0 spins, bounded) until the rows of instance `inst` have landed; warp-uniform
@@ -82,6 +89,26 @@ __device__ __forceinline__ void stream_wait(const KParams &P, long long inst)
 __device__ __forceinline__ int4 load_row(const KParams &P, long long r)
 {
     return P.stream_ready ? __ldcg(P.req + r) : P.req[r];
+}
+
+// Rows k0 + lane (k = that, all 32 lanes call it together) of an instance in SCHED_REQ_P16
+// form ({o-1:6 | s-1:3 | gap:7}, a_(-1) = 0, o~ = o; include/kvsched.h): a_k is the prefix
+// sum of the gaps, `carry` = a of the row before k0 (0 for the first chunk; updated).  Rows
+// k >= n decode as gap 0.  Read past L1: the rows may still be landing.
+__device__ __forceinline__ int4 load_row_p16(const KParams &P, long long off, int k, int n, int &carry)
+{
+    const int lane = lane_id();
+    const uint32_t v = k < n ? (uint32_t)__ldcg(reinterpret_cast<const unsigned short *>(P.req16) + off + k) : 0u;
+    int a = (int)(v >> 9);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(KV_FULL, a, d);
+        if (lane >= d) a += y;
+    }
+    a += carry;
+    carry = __shfl_sync(KV_FULL, a, 31);
+    const int o = (int)(v & 63u) + 1;
+    return make_int4(a, (int)((v >> 6) & 7u) + 1, o, o);
 }
 
 // the instance's outputs are written: count it for its chunk's release
@@ -116,6 +143,7 @@ __device__ __forceinline__ void fill_unscheduled(const KParams &P, long long off
     for (int k = lane_id(); k < n; k += 32) {
         if (P.completion) P.completion[off + k] = -1;
         if (P.start) P.start[off + k] = -1;
+        if (P.lat16) P.lat16[off + k] = 0xffffu;
     }
 }
 

@@ -683,6 +683,40 @@ def test_host_path_lane_chunks(K, ctx, oracle_mod, pol, monkeypatch):
     assert np.array_equal(outs["latency16"], _expected_latency16(o, b))
 
 
+@pytest.mark.parametrize("chunks", [1, 5, 16, 97])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_host_path_streamed(K, ctx, oracle_mod, pol, chunks, monkeypatch):
+    """The streamed host path (P16 rows, MC policies on the lane path): one persistent lane
+    launch decodes the wire rows itself as the chunks land (flags set by stream memory
+    operations), size-scope instances (n > 96) beside it on the side stream, row-scope ones
+    (s = 8) after it, chunk k copied out once its instances are counted.  Every output, the
+    latency16 conversion, and byte equality with the chunked pipeline (KVSCHED_HOST_STREAM=0)."""
+    import paper_2502_07115_b200.kvsched as kv
+    monkeypatch.setenv("KVSCHED_HOST_STREAM_CHUNKS", str(chunks))
+    b = _concat(W.am2(2500, 150 + pol), W.lane_mix(400, 151 + pol, n_max=130, s_max=8, gap_max=30))
+    b = _concat(b, W.from_instances([([[0, 5, 6, 6]], 10), ([[0, 1, 1, 1], [0, 8, 2, 2]], 10)]))
+    pk = b.packed_p16()
+    assert pk is not None
+    o = oracle_run(oracle_mod, b, pol)
+    want = _expected_latency16(o, b)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("KVSCHED_HOST_STREAM", mode)
+        outs = _host_outputs(b)
+        outs["latency16"] = np.empty(b.n_req, np.uint16)
+        ctx.run_host(b.offset, pk, b.mem, K.Policy(KIND[pol]), outs, hints=K.hints_of(b), req_format=kv.REQ_P16)
+        assert ("streamed" in ctx.last_kernel()) == (mode == "1"), ctx.last_kernel()
+        assert_parity(o, outs, b, f"host streamed={mode}")
+        assert np.array_equal(outs["latency16"], want), mode
+        res[mode] = outs
+        outs2 = {k: np.empty_like(v) for k, v in outs.items() if k not in ("completion", "start")}
+        ctx.run_host(b.offset, pk, b.mem, K.Policy(KIND[pol]), outs2, hints=K.hints_of(b), req_format=kv.REQ_P16)
+        assert np.array_equal(outs2["latency16"], want), mode
+        assert np.array_equal(outs2["tel"], np.asarray(o["tel"])), mode
+    for k in res["1"]:
+        assert np.array_equal(res["1"][k], res["0"][k]), k
+
+
 def test_host_path(K, ctx, oracle_mod):
     """sched_run_instances_host (host buffers, copies inside the call) gives the same bytes."""
     import paper_2502_07115_b200.kvsched as kv
