@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(256) k_mc_prep_w(const KParams P, uint4 *rq_ea
 // ---------------------------------------------------------------------------------------
 // k_mc_ring: the round loop
 // ---------------------------------------------------------------------------------------
-template <int POL>
+// QREG (instances of at most 1024 requests): the waiting queue is one bitmap word per lane in
+// a register (lane l: ranks 32l .. 32l+31) instead of the two-level shared-memory bitmap;
+// arrivals stage their bits through smq (shared atomics) and each lane folds its word in.
+template <int POL, bool QREG>
 __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, uint32_t *bm, uint32_t *smq,
                                 Stage &A)
 {
@@ -578,6 +581,7 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
     smq[lane] = 0u;
     __syncwarp();
     WarpQueue Q{bm, smq, (nw + 31) >> 5};
+    uint32_t qw = 0u, qhw = 0u;                            // QREG: this lane's word, the head's word
     stage_begin(A, P.arr8, off, n);
     const bool multi = !(P.flags & 1);
 
@@ -626,11 +630,19 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
             int rk = KV_INF;
             if (take) {
                 rk = e.y;
-                q_insert(Q, rk);
+                if (QREG) atomicOr(&smq[rk >> 5], 1u << (rk & 31));
+                else q_insert(Q, rk);
                 suma += e.x;
             }
             const int mn = warp_min_i32(rk);
             if (mn < h) { h = mn; hstale = true; head_fits = false; }
+            if (QREG) {                                    // fold the staged bits in
+                __syncwarp();
+                qw |= smq[lane];
+                smq[lane] = 0u;
+                __syncwarp();
+                qhw = __shfl_sync(KV_FULL, qw, (h >> 5) & 31);
+            }
             next += cnt;
             a_next = cnt < 32 ? __shfl_sync(KV_FULL, e.x, cnt & 31) : (next < n ? t : KV_INF);
         }
@@ -660,14 +672,28 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
                 }
             }
             head_fits = false;
-            // MC-SF: the next head leaves the queue first so that its entry loads while the
-            // ramp is written (a RETRY restarts the instance, so the order is free)
-            int hn = KV_INF;
-            uint2 hen = he;
-            if (POL == POL_MCSF) {
+            // the next head leaves the queue first so that its entry loads while the ramp is
+            // written (a RETRY restarts the instance, so the order is free; MC-Benchmark too).
+            // Fusing the ramp with the next head's window pass measured slower (C4 7.47 ->
+            // 8.0 ms: the pass must wait for that entry's load)
+            int hn;
+            if (QREG) {
+                const uint32_t bit = 1u << (h & 31);
+                if (lane == (h >> 5)) qw &= ~bit;
+                qhw &= ~bit;
+                if (qhw) {
+                    hn = (h & ~31) + __ffs(qhw) - 1;       // the rest of the head's word is > h
+                } else {
+                    const uint32_t b = __ballot_sync(KV_FULL, qw != 0u);
+                    const int l0 = b ? __ffs(b) - 1 : 0;
+                    qhw = __shfl_sync(KV_FULL, qw, l0);
+                    hn = b ? (l0 << 5) + __ffs(qhw) - 1 : KV_INF;
+                }
+            } else {
                 hn = q_pop_head(Q, h);
-                if (hn != KV_INF) hen = rq8[hn];
             }
+            uint2 hen = he;
+            if (hn != KV_INF) hen = rq8[hn];
             r16_ramp(R, t, w, s);
             if (w > L && !long_add(G, t, s, t + w, idx)) { status = ST_RETRY; break; }
             const int c = t + w;                           // o = w on this path
@@ -678,10 +704,6 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
             sumc += c;
             maxc = max(maxc, c);
             __syncwarp();
-            if (POL != POL_MCSF) {
-                hn = q_pop_head(Q, h);
-                if (hn != KV_INF) hen = rq8[hn];
-            }
             h = hn;
             if (h == KV_INF) break;
             he = hen;
@@ -719,7 +741,7 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
             if (P.start) P.start[off + k] = -1;
         }
         for (int w = lane; w < nw; w += 32) {
-            uint32_t bits = bm[w];
+            uint32_t bits = QREG ? qw : bm[w];
             while (bits) {
                 const int r = (w << 5) + __ffs(bits) - 1;
                 bits &= bits - 1;
@@ -743,7 +765,7 @@ __device__ void mcring_instance(const KParams &P, long long inst, const R16 &R, 
 #ifndef KV_MCRING_MINB
 #define KV_MCRING_MINB 8        // blocks of 4 warps per SM the register budget must allow
 #endif
-template <int POL>
+template <int POL, bool QREG = false>
 __global__ void __launch_bounds__(128, KV_MCRING_MINB) k_mc_ring(const KParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -775,7 +797,7 @@ __global__ void __launch_bounds__(128, KV_MCRING_MINB) k_mc_ring(const KParams P
     while (w < n_work) {
         long long nxt = 0;
         if (lane == 0) nxt = atomicAdd(P.counter, 1ull);
-        mcring_instance<POL>(P, P.work_list ? P.work_list[w] : w, R, bm, smq, A);
+        mcring_instance<POL, QREG>(P, P.work_list ? P.work_list[w] : w, R, bm, smq, A);
         w = __shfl_sync(KV_FULL, nxt, 0);
         __syncwarp();
     }

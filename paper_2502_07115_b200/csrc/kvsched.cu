@@ -1057,6 +1057,12 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
                 wps = mcring_wps;
             }
             name = pol->policy == SCHED_MCSF ? "k_mc_ring<MCSF>" : "k_mc_ring<MCBENCH>";
+#ifndef KV_MCRING_QREG
+#define KV_MCRING_QREG 1
+#endif
+            if (KV_MCRING_QREG && Q.NP <= 1024)        // the waiting queue in registers
+                return pol->policy == SCHED_MCSF ? launch_sim(c, k_mc_ring<POL_MCSF, true>, Q, Q.warp_bytes, name, wps)
+                                                 : launch_sim(c, k_mc_ring<POL_MCBENCH, true>, Q, Q.warp_bytes, name, wps);
             return pol->policy == SCHED_MCSF ? launch_sim(c, k_mc_ring<POL_MCSF>, Q, Q.warp_bytes, name, wps)
                                              : launch_sim(c, k_mc_ring<POL_MCBENCH>, Q, Q.warp_bytes, name, wps);
         }
