@@ -1006,7 +1006,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             c->launches++;
         }
         if (max_req > KV_PREP_WARP_N) {   // larger instances: one CTA each
-            const int ssmem = early ? next_pow2(max_req) * 4 : 16;
+            const int ssmem = early ? next_pow2(max_req) * 4 + (int)kPrepSortBytes + 16 : 16;
             auto prep = early ? k_mc_prep<POL_MCSF> : k_mc_prep<POL_MCBENCH>;
             CUDA_TRY(c, cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
             int per_sm = 1;
