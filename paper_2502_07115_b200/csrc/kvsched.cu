@@ -1376,14 +1376,17 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
             CUDA_TRY(c, cudaEventRecord(ev[1], c->s_in));           // offsets and budgets are in
             const long long *doff = (const long long *)c->h_off.p;
             const uint16_t *d16 = reinterpret_cast<const uint16_t *>(c->h_pk.p);
-            for (long long k = 0; k < K; ++k) {
-                const long long i0 = k * C, i1 = std::min(ni, i0 + C);
-                const long long r0 = hoff[i0], r1 = hoff[i1];
+            // copy-in in groups of flag chunks growing from 1 to gmax (one copy, then a flag
+            // per chunk): the first rows land early, the later copies are large
+            for (long long k = 0, gs = 1; k < K; k += gs, gs = std::min(2 * gs, gmax)) {
+                const long long ke = std::min(K, k + gs);
+                const long long r0 = hoff[k * C], r1 = hoff[std::min(ni, ke * C)];
                 if (r1 > r0)
                     CUDA_TRY(c, cudaMemcpyAsync((char *)c->h_pk.p + r0 * 2, (const char *)inst->req + r0 * 2,
                                                 (size_t)(r1 - r0) * 2, cudaMemcpyHostToDevice, c->s_in));
-                if (g_write32((CUstream)c->s_in, (CUdeviceptr)(ready + k), 1u, 0) != CUDA_SUCCESS)
-                    return fail(c, SCHED_E_CUDA, "cuStreamWriteValue32 failed");
+                for (long long j = k; j < ke; ++j)
+                    if (g_write32((CUstream)c->s_in, (CUdeviceptr)(ready + j), 1u, 0) != CUDA_SUCCESS)
+                        return fail(c, SCHED_E_CUDA, "cuStreamWriteValue32 failed");
                 mark("in", c->s_in);
             }
             // the simulation: one launch over everything, gated per chunk
