@@ -171,7 +171,9 @@ typedef struct {
     uint16_t *latency16;        /* [n_req] compact schedule for transfers: c_i - a_i when the
                                    request completed and c_i - a_i <= 65534, else 65535
                                    (completion = a_i + latency16).  Computed on the device
-                                   from the completion rounds after the run (ABI version 2). */
+                                   from the completion rounds after the run, or written by
+                                   the kernels themselves on the streamed host path (ABI
+                                   version 2).                                              */
 } sched_outputs;
 
 /* Create a context on `device` that enqueues on `cuda_stream` (a cudaStream_t; NULL = the
@@ -183,9 +185,10 @@ int sched_set_stream(sched_ctx *ctx, void *cuda_stream);
 
 /* Simulate every instance of `inst` under `pol` (device pointers), on persistent grids.
  * MC policies with M <= 64: one LANE per instance (byte-profile kernel k_mc_lane for n <= 96,
- * k_mc_flat for larger simultaneous-arrival instances), the rest one warp per instance
- * (k_mc_small); every other budget / policy: the shared-memory ring kernels (k_ring, k_prot)
- * ("Kernels").  Per-instance data errors set that instance's status only.
+ * k_mc_flatq -- one instance per 8-lane group -- for larger simultaneous-arrival instances),
+ * the rest one warp per instance (k_mc_small); MC policies with 64 < M <= 32767: one warp per
+ * instance on a 16-bit profile ring (k_mc_prep + k_mc_ring); the alpha policies and larger
+ * budgets: the 32-bit ring kernels (k_ring, k_prot) ("Kernels").  Per-instance data errors set that instance's status only.
  * Returns SCHED_E_ARG (nothing enqueued) for bad arguments, including an unknown policy or
  * flag, alpha outside [0, 1), or beta_thresh outside [1, 2^32] for SCHED_ALPHA_BETA.      */
 int sched_run_instances(sched_ctx *ctx, const sched_instances *inst, const sched_policy *pol,

@@ -65,12 +65,25 @@ def main():
             # the request-row format and entry point: int32 rows on the device, a packed
             # format when the batch encodes (decoded on the device, + latency16), or the
             # host-buffer entry point (pipelined copies and kernels)
-            mode = str(g.choice(["i32", "u16", "u8", "p16", "host"]))
-            if mode in ("u16", "u8", "p16"):
-                pk = {"u8": b.packed_u8, "p16": b.packed_p16, "u16": b.packed_u16}[mode]()
+            mode = str(g.choice(["i32", "u16", "u8", "p16", "host", "hostp16"]))
+            if mode in ("u16", "u8", "p16", "hostp16"):
+                pk = {"u8": b.packed_u8, "p16": b.packed_p16, "u16": b.packed_u16, "hostp16": b.packed_p16}[mode]()
                 if pk is None:
                     mode = "i32"
-            if mode == "host":
+            if mode == "hostp16":
+                # the host entry point with P16 rows: the streamed pipeline for MC policies
+                # (M <= 64), flag chunk count drawn too; the chunked pipeline otherwise
+                import os
+                os.environ["KVSCHED_HOST_STREAM_CHUNKS"] = str(int(g.choice([1, 3, 16, 64])))
+                r = {"completion": np.empty(b.n_req, np.int32), "start": np.empty(b.n_req, np.int32),
+                     "latency16": np.empty(b.n_req, np.uint16)}
+                for k in ("tel", "rounds", "decision_rounds", "evictions"):
+                    r[k] = np.empty(b.n_inst, np.int64)
+                for k in ("makespan", "peak_mem", "status"):
+                    r[k] = np.empty(b.n_inst, np.int32)
+                ctx.run_host(b.offset, pk, b.mem, p, r, hints=K.hints_of(b), req_format=K.kvsched.REQ_P16)
+                mode = "hp16" + ("s" if "streamed" in ctx.last_kernel() else "c")
+            elif mode == "host":
                 r = {"completion": np.empty(b.n_req, np.int32), "start": np.empty(b.n_req, np.int32)}
                 for k in ("tel", "rounds", "decision_rounds", "evictions"):
                     r[k] = np.empty(b.n_inst, np.int64)
