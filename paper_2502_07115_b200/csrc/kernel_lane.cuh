@@ -141,7 +141,8 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
     const long long off = __shfl_sync(KV_FULL, F.off, F.cur);
     const int n = __shfl_sync(KV_FULL, F.n, F.cur);
     const int m = n <= LANE_NP ? n : 0;          // out-of-scope sizes are not staged
-    if (P.stream_ready && m > 0) {               // chunks land in order: poll a new one only
+    if (R16 && P.stream_ready && m > 0) {        // (streamed host path only) chunks land in
+                                                 // order: poll a new one only
         const long long id = __shfl_sync(KV_FULL, F.id, F.cur);
         const int ch = (int)(id / P.stream_chunk);
         if (ch > F.rdy) {
