@@ -144,7 +144,7 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
     if (R16 && P.stream_ready && m > 0) {        // (streamed host path only) chunks land in
                                                  // order: poll a new one only
         const long long id = __shfl_sync(KV_FULL, F.id, F.cur);
-        const int ch = (int)(id / P.stream_chunk);
+        const int ch = (int)((unsigned)id / (unsigned)P.stream_chunk);
         if (ch > F.rdy) {
             stream_wait(P, id);
             F.rdy = ch;
@@ -163,7 +163,7 @@ __device__ __forceinline__ void feed_prefetch(const KParams &P, LaneFeed &F)
 #pragma unroll
     for (int c = 0; c < LANE_NC; ++c) {
         const int k = lane + 32 * c;
-        F.r[c] = k < m ? load_row(P, off + k) : make_int4(0x3fffffff, 1, 1, 1);
+        F.r[c] = k < m ? P.req[off + k] : make_int4(0x3fffffff, 1, 1, 1);   // (device path: rows resident)
     }
 }
 
@@ -327,7 +327,7 @@ __device__ __forceinline__ bool lane_refill(const KParams &P, uint32_t *data, in
     return true;
 }
 
-template <int NW>
+template <int NW, bool R16>
 __device__ __forceinline__ void lane_write_result(const KParams &P, const LaneInst<NW> &L)
 {
     if (P.tel) P.tel[L.inst] = L.sumc - L.suma;
@@ -337,7 +337,7 @@ __device__ __forceinline__ void lane_write_result(const KParams &P, const LaneIn
     if (P.makespan) P.makespan[L.inst] = L.maxc;
     if (P.peak) P.peak[L.inst] = L.peak;
     if (P.status) P.status[L.inst] = ST_OK;
-    if (P.stream_done) stream_count(P, L.inst);
+    if (R16 && P.stream_done) stream_count(P, L.inst);
 }
 
 // max over the profile bytes, as 16x2 halves (values <= 64)
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(128, 4) k_mc_lane(const KParams P)
                     if (L.dec) { ++L.dr; L.nr += max(0, L.maxc - L.t - 1); }
                     else L.nr += max(0, L.maxc - L.t);
                     L.peak = max(L.peak, hmax16(pk16));
-                    lane_write_result(P, L);
+                    lane_write_result<NW, R16>(P, L);
                     L.active = false;
                 } else if (L.maxc <= L.t) {                  // S and R empty: idle until a_next
                     L.t = L.a_next;                          // (the profile is all zero)

@@ -1335,6 +1335,7 @@ int sched_run_instances_host(sched_ctx *c, const sched_instances *inst, const sc
                                hi.max_requests <= kSmallMaxRequests && pol->round_cap <= 0 &&
                                !(pol->flags & (SCHED_FLAG_PER_ROUND | SCHED_FLAG_WARP_PER_INSTANCE));
         if (lane_path && inst->req_format == SCHED_REQ_P16 && !(se && se[0] == '0') && !c->stream_off && ni >= 64 &&
+            ni < (1ll << 31) &&                                  // 32-bit chunk arithmetic in the kernels
             stream_mem_ops(c)) {
             // K flag chunks (copy-in granularity); the copy-out takes them in groups that grow
             // from one chunk to KVSCHED_HOST_STREAM_GROUP (the first results leave early, the

@@ -74,7 +74,7 @@ __device__ __forceinline__ void stream_wait(const KParams &P, long long inst)
 {
     if (!P.stream_ready) return;
     if (lane_id() == 0) {
-        const volatile int *f = P.stream_ready + inst / P.stream_chunk;
+        const volatile int *f = P.stream_ready + (unsigned)inst / (unsigned)P.stream_chunk;   // (ni < 2^31)
         long long spins = 0;
         while (*f == 0) {
             __nanosleep(200);
@@ -115,7 +115,7 @@ __device__ __forceinline__ int4 load_row_p16(const KParams &P, long long off, in
 __device__ __forceinline__ void stream_count(const KParams &P, long long inst)
 {
     __threadfence();
-    atomicAdd(P.stream_done + inst / P.stream_chunk, 1u);
+    atomicAdd(P.stream_done + (unsigned)inst / (unsigned)P.stream_chunk, 1u);   // (ni < 2^31 when streamed)
 }
 
 // Lane 0 writes the per-instance outputs.
