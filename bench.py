@@ -418,6 +418,9 @@ def main():
                 kernel_share_of_step=(k_tot_ms / args.steps) / (ms_max / args.steps) if args.steps else None,
                 kernels={k: {"ms_per_step": v[0] / max(args.steps, 1), "launches_per_step": v[1] / max(args.steps, 1)}
                          for k, v in kst.items()},
+                kernels_note="CUDA events bracket each launch on its own stream: the side-stream fallbacks "
+                             "(k_mc_flatq / k_mc_small beside k_mc_lane, usually an empty or ~1 % list) include "
+                             "the wait for SMs held by the main kernel; per-launch work is in the ncu launch list",
                 hbm=hbm, issue=issue_roofline(rec, f_mhz) if same_launch else None)
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
