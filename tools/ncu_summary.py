@@ -34,9 +34,9 @@ POLICY = {"0": "MCSF", "1": "MCBENCH", "2": "ALPHA", "3": "ALPHA_BETA"}
 
 def abi_name(short: str) -> str:
     """ncu's demangled template name -> the name sched_last_kernel() reports."""
-    m = re.match(r"k_mc_(lane|flat)<(\d), (\d+)>", short)
+    m = re.match(r"k_mc_(lane|flat)<(\d), (\d+)(?:, (\d))?>", short)
     if m:
-        return f"k_mc_{m.group(1)}<{POLICY[m.group(2)]}>"
+        return f"k_mc_{m.group(1)}<{POLICY[m.group(2)]}" + (",p16>" if m.group(4) == "1" else ">")
     m = re.match(r"k_mc_small<(\d), (\d), (\d)>", short)
     if m:
         pol, multi, qreg = m.groups()
