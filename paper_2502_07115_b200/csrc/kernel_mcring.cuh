@@ -42,6 +42,9 @@ namespace kv {
 #ifndef KV_PREP_RADIX
 #define KV_PREP_RADIX 1                      // k_mc_prep: CUB block radix sort for 2048 <= NP <= 16384
 #endif
+#ifndef KV_PREP_CTA_LO
+#define KV_PREP_CTA_LO 128                   // instances of KV_PREP_CTA_LO < n <= 1024: k_mc_prep<POL, 256>
+#endif                                       // (KV_PREP_CTA_LO >= 1024: all on k_mc_prep_w)
 #define KV_STAGE_CH 32                       // arrival entries per staged chunk
 #define KV_STAGE_SLOTS 4                     // chunks resident / in flight per warp
 #define KV_STAGE_ENTRIES (KV_STAGE_CH + 2)   // one extra on each side for 16-byte alignment
@@ -339,11 +342,12 @@ __device__ __forceinline__ uint32_t work_estimate(int a0, int alast, long long v
 // block radix sort on the o~ bits only (stable, so ties stay in idx order, P:175 / Q5):
 // ceil(bits / 4) passes instead of the bitonic network's log2(NP) (log2(NP) + 1) / 2 stages
 // with a block barrier each.  Blocked arrangement: thread t holds keys t IT .. t IT + IT - 1.
-template <int IT>
-using PrepSort = cub::BlockRadixSort<uint32_t, 1024, IT>;
-constexpr size_t kPrepSortBytes = sizeof(typename PrepSort<16>::TempStorage);
+template <int BLOCK, int IT>
+using PrepSort = cub::BlockRadixSort<uint32_t, BLOCK, IT>;
+constexpr size_t kPrepSortBytes = sizeof(typename PrepSort<1024, 16>::TempStorage);      // 1024 threads
+constexpr size_t kPrepSortBytes256 = sizeof(typename PrepSort<256, 4>::TempStorage);     // 256 threads
 
-template <int IT>
+template <int BLOCK, int IT>
 __device__ __forceinline__ void prep_radix_sort(uint32_t *keys, int n, int max_len, void *tmp)
 {
     const int tid = threadIdx.x;
@@ -355,7 +359,7 @@ __device__ __forceinline__ void prep_radix_sort(uint32_t *keys, int n, int max_l
     }
     __syncthreads();
     const int eb = min(32, 15 + (32 - __clz(max(max_len, 1))));
-    PrepSort<IT>(*reinterpret_cast<typename PrepSort<IT>::TempStorage *>(tmp)).Sort(k, 15, eb);
+    PrepSort<BLOCK, IT>(*reinterpret_cast<typename PrepSort<BLOCK, IT>::TempStorage *>(tmp)).Sort(k, 15, eb);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < IT; ++j) keys[tid * IT + j] = k[j];
@@ -365,8 +369,10 @@ __device__ __forceinline__ void prep_radix_sort(uint32_t *keys, int n, int max_l
 // ---------------------------------------------------------------------------------------
 // k_mc_prep: validation, round cap, ranks, the rq8 / arr8 streams (one CTA per instance)
 // ---------------------------------------------------------------------------------------
-template <int POL>
-__global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_early, int *arank_early)
+// BLOCK = 1024 takes the instances with more than 1024 requests; BLOCK = 256 those with
+// n_lo < n <= 1024 (a CTA radix sort instead of k_mc_prep_w's warp bitonic network).
+template <int POL, int BLOCK = 1024>
+__global__ void __launch_bounds__(BLOCK) k_mc_prep(const KParams P, uint4 *rq_early, int *arank_early, int n_lo = 0)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem_raw);
@@ -377,7 +383,9 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
     for (long long inst = blockIdx.x; inst < P.n_inst; inst += gridDim.x) {
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
-        if (n <= KV_PREP_WARP_N) continue;                // k_mc_prep_w
+        // another prep's instance (instances above the caller's size hint are k_mc_prep_w's:
+        // the launches are sized from the hint)
+        if ((BLOCK == 1024 ? n <= KV_PREP_WARP_N : (n <= n_lo || n > KV_PREP_WARP_N)) || n > P.max_requests) continue;
         const int M = P.mem[inst];
         if (tid == 0) {
             s_flags = (n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows) ? 2 : 0;
@@ -433,12 +441,17 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
             if (tid < 32) write_result(P, inst, InstResult{0, 0, 0, 0, 0, 0, ST_UNSUPPORTED});
         } else {
             const int NPr = next_pow2(n);
-            if (POL == POL_MCSF && KV_PREP_RADIX && NPr >= 2048 && NPr <= 16384) {   // block radix sort
+            if (POL == POL_MCSF && KV_PREP_RADIX && BLOCK == 1024 && NPr >= 2048 && NPr <= 16384) {   // block radix sort
                 void *tmp = smem_raw + (size_t)P.NP * 4;
-                if (NPr == 2048) prep_radix_sort<2>(keys, n, P.max_len, tmp);
-                else if (NPr == 4096) prep_radix_sort<4>(keys, n, P.max_len, tmp);
-                else if (NPr == 8192) prep_radix_sort<8>(keys, n, P.max_len, tmp);
-                else prep_radix_sort<16>(keys, n, P.max_len, tmp);
+                if (NPr == 2048) prep_radix_sort<BLOCK, 2>(keys, n, P.max_len, tmp);
+                else if (NPr == 4096) prep_radix_sort<BLOCK, 4>(keys, n, P.max_len, tmp);
+                else if (NPr == 8192) prep_radix_sort<BLOCK, 8>(keys, n, P.max_len, tmp);
+                else prep_radix_sort<BLOCK, 16>(keys, n, P.max_len, tmp);
+            } else if (POL == POL_MCSF && BLOCK == 256 && NPr >= 256 && NPr <= 1024) {
+                void *tmp = smem_raw + (size_t)P.NP * 4;
+                if (NPr == 256) prep_radix_sort<256, 1>(keys, n, P.max_len, tmp);
+                else if (NPr == 512) prep_radix_sort<256, 2>(keys, n, P.max_len, tmp);
+                else prep_radix_sort<256, 4>(keys, n, P.max_len, tmp);
             } else if (POL == POL_MCSF) {                   // bitonic sort of (o~, idx) keys
                 const int NPi = next_pow2(n);
                 for (int k = n + tid; k < NPi; k += blockDim.x) keys[k] = 0xffffffffu;
@@ -491,7 +504,8 @@ __global__ void __launch_bounds__(1024) k_mc_prep(const KParams P, uint4 *rq_ear
 // (keys in 4 KB of shared memory per warp, the bitonic stages separated by __syncwarp
 // instead of block barriers); k_mc_prep then takes only the larger instances.
 template <int POL>
-__global__ void __launch_bounds__(256) k_mc_prep_w(const KParams P, uint4 *rq_early, int *arank_early)
+__global__ void __launch_bounds__(256) k_mc_prep_w(const KParams P, uint4 *rq_early, int *arank_early,
+                                                   int n_hi = KV_PREP_WARP_N)
 {
     __shared__ __align__(16) uint32_t keys_all[8][KV_PREP_WARP_N];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -501,7 +515,7 @@ __global__ void __launch_bounds__(256) k_mc_prep_w(const KParams P, uint4 *rq_ea
     for (long long inst = (long long)blockIdx.x * 8 + warp; inst < P.n_inst; inst += nwarps) {
         const long long off = P.offset[inst] - P.row_base;
         const int n = (int)(P.offset[inst + 1] - P.offset[inst]);
-        if (n > KV_PREP_WARP_N) continue;                  // k_mc_prep
+        if (n > n_hi && n <= P.max_requests) continue;     // k_mc_prep (hint violators: here)
         const int M = P.mem[inst];
         int fl = (n > P.max_requests || M > P.max_mem || off + n > P.scratch_rows) ? 2 : 0;
         long long so = 0, vol = 0;

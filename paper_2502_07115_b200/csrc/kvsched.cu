@@ -994,14 +994,33 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         }
         uint4 *rq_e = reinterpret_cast<uint4 *>(c->rq.p);
         int *ar_e = reinterpret_cast<int *>(c->arank.p);
-        {   // instances of <= KV_PREP_WARP_N requests: one warp each
+        // MC-SF instances of KV_PREP_CTA_LO < n <= KV_PREP_WARP_N requests: one 256-thread CTA
+        // each (CUB block radix sort of the keys); smaller ones (and MC-Benchmark, which sorts
+        // nothing): one warp each
+        const int w_hi = early && KV_PREP_CTA_LO < KV_PREP_WARP_N ? KV_PREP_CTA_LO : KV_PREP_WARP_N;
+        {   // instances of <= w_hi requests: one warp each
             auto prep_w = early ? k_mc_prep_w<POL_MCSF> : k_mc_prep_w<POL_MCBENCH>;
             int per_sm = 1;
             CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_w, 256, 0));
             long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
             const long long need = (inst->n_instances + 7) / 8;
             if (blocks > need) blocks = need > 0 ? need : 1;
-            prep_w<<<(int)blocks, 256, 0, c->stream>>>(P, rq_e, ar_e);
+            prep_w<<<(int)blocks, 256, 0, c->stream>>>(P, rq_e, ar_e, w_hi);
+            CUDA_TRY(c, cudaGetLastError());
+            c->launches++;
+        }
+        if (w_hi < KV_PREP_WARP_N && max_req > w_hi) {
+            const int ssmem = next_pow2(max_req < 256 ? 256 : std::min(max_req, KV_PREP_WARP_N)) * 4 +
+                              (int)kPrepSortBytes256 + 16;
+            auto prep = k_mc_prep<POL_MCSF, 256>;
+            CUDA_TRY(c, cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+            int per_sm = 1;
+            CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 256, ssmem));
+            long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
+            if (blocks > inst->n_instances) blocks = inst->n_instances > 0 ? inst->n_instances : 1;
+            KParams Q = P;
+            Q.NP = ssmem > 0 ? next_pow2(max_req < 256 ? 256 : std::min(max_req, KV_PREP_WARP_N)) : P.NP;   // keys region
+            prep<<<(int)blocks, 256, ssmem, c->stream>>>(Q, rq_e, ar_e, w_hi);
             CUDA_TRY(c, cudaGetLastError());
             c->launches++;
         }
@@ -1013,7 +1032,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
             CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 1024, ssmem));
             long long blocks = (long long)(per_sm > 0 ? per_sm : 1) * c->num_sms;
             if (blocks > inst->n_instances) blocks = inst->n_instances > 0 ? inst->n_instances : 1;
-            prep<<<(int)blocks, 1024, ssmem, c->stream>>>(P, rq_e, ar_e);
+            prep<<<(int)blocks, 1024, ssmem, c->stream>>>(P, rq_e, ar_e, 0);
             CUDA_TRY(c, cudaGetLastError());
             c->launches++;
         }

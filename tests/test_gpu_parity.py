@@ -869,6 +869,26 @@ def test_hint_violation_does_not_spill_scratch(K, ctx, oracle_mod, pol):
         assert np.array_equal(g["completion"][lo:hi], o["completion"][lo:hi]), k
 
 
+@pytest.mark.parametrize("pol", [0, 1])
+@pytest.mark.parametrize("big_n", [200, 700, 1500])
+def test_hint_violation_any_prep_size(K, ctx, oracle_mod, pol, big_n):
+    """An instance above the caller's max_requests hint is UNSUPPORTED whichever prep kernel
+    its size would select (warp, 256-thread CTA, 1024-thread CTA): the launches are sized
+    from the hint, so k_mc_prep_w takes every violator."""
+    big = ([[0, 1, 5, 5]] * big_n, 300)
+    rest = W.random_small(40, 28, n_max=15, M_lo=70, M_hi=200, a_max=20)
+    b = W.from_instances([big] + [rest.instance(k) for k in range(rest.n_inst)] + [big])
+    g = gpu_run(K, ctx, b, pol, hints=(20, 300, 63))
+    o = oracle_run(oracle_mod, b, pol)
+    assert g["status"][0] == 3 and g["status"][-1] == 3
+    for k in range(1, b.n_inst - 1):
+        if g["status"][k] == 3:
+            continue
+        lo, hi = b.offset[k], b.offset[k + 1]
+        assert g["status"][k] == o["status"][k] and g["tel"][k] == o["tel"][k], k
+        assert np.array_equal(g["completion"][lo:hi], o["completion"][lo:hi]), k
+
+
 def test_lane_scope_far_arrivals(K, ctx, oracle_mod):
     """Arrival rounds near 2^30: the default cap min(2^30, ...) is reachable, so the lane and
     flat kernels must hand such instances to the general kernel."""
