@@ -478,6 +478,10 @@ def main():
         lat = host["latency16"][:batch.n_req].view(np.uint16).astype(np.int64)
         same = bool(np.array_equal(host["rounds"][:batch.n_inst], out["rounds"][:batch.n_inst].cpu().numpy())
                     and np.array_equal(batch.req[:, 0].astype(np.int64) + lat, comp_dev))
+        if world > 1:                     # every rank's host-path results against its device run
+            ok_t = torch.tensor([1 if same else 0], dtype=torch.int64, device=dev)
+            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+            same = bool(ok_t.item())
         h2d = rows.nbytes + (batch.n_inst + 1) * 8 + batch.n_inst * 4
         d2h = sum(v.numel() * v.element_size() for v in h_out.values())
         e2e = {"value": rounds_all * args.e2e_steps / (e_ms / 1000.0), "unit": UNIT,

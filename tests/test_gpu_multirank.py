@@ -28,10 +28,12 @@ def _free_port():
     return p
 
 
-def _bench(tmp, nproc, extra, name):
+def _bench(tmp, nproc, extra, name, e2e=False):
     dump = tmp / f"{name}.npy"
-    args = ["bench.py", "--gpus", str(nproc), "--steps", "2", "--warmup", "3", "--no-e2e", "--no-also",
+    args = ["bench.py", "--gpus", str(nproc), "--steps", "2", "--warmup", "3", "--no-also",
             "--no-cpu-baseline", "--dump-results", str(dump), *extra]
+    if not e2e:
+        args.append("--no-e2e")
     env = dict(os.environ, KVSCHED_BENCH_ONE_GPU="1", KVSCHED_BENCH_BACKEND="gloo")
     if nproc > 1:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
@@ -66,3 +68,15 @@ def test_weak_split_runs_every_rank(tmp_path):
     line, r2 = _bench(tmp_path, 2, extra, "two")
     assert line["scaling"] == "weak" and line["config"]["instances_total"] == 10_000
     assert r2.shape[1] == 10_000 and np.array_equal(r2[:, :5000], r1)
+
+
+def test_streamed_host_path_per_rank(tmp_path):
+    """The e2e leg at N > 1: every rank runs its shard through sched_run_instances_host (P16
+    rows: the streamed pipeline) and checks it against its device-path run
+    (matches_device_run); rank 0 reports, the gathered device results equal the 1-rank run."""
+    extra = ["--workload", "c5", "--instances", "20000", "--e2e-steps", "2"]
+    one, r1 = _bench(tmp_path, 1, extra, "one", e2e=True)
+    assert one["e2e"]["matches_device_run"] and one["e2e"]["req_format"] == "p16"
+    line, r2 = _bench(tmp_path, 2, extra, "two", e2e=True)
+    assert line["e2e"]["matches_device_run"]
+    assert np.array_equal(r2, r1)
