@@ -896,7 +896,7 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
         const int v = atoi(e);
         if (v >= 64 && (v & (v - 1)) == 0) ring_short = v;
     }
-    const int L_short = L_full < ring_short ? L_full : ring_short;
+    int L_short = L_full < ring_short ? L_full : ring_short;
     P.L = L_short;
     const bool prot = pol->policy >= SCHED_MCSF_PROTECTED;
     // MC policies with M <= 32767: the 16-bit profile ring with staged arrivals
@@ -906,6 +906,25 @@ static int run_impl(sched_ctx *c, const sched_instances *inst, const sched_polic
     auto wbytes = [&](int L) {
         return mcr ? mcring_warp_bytes(L, P.NP) : prot ? prot_warp_bytes(L, P.NP) : ring_warp_bytes(L, P.NP, pol->policy);
     };
+    // MC ring path, batches under two full waves (the launch keeps 16 resident warps per SM,
+    // launch_sim): those 16 warps fit a 4096-slot window, so fewer long requests take the
+    // per-position path past the ring (C3: 28.9 -> 26.6-27.0 ms; the full-occupancy batches of
+    // C4 keep 2048, where a larger window would halve the resident warps)
+    if (mcr && !getenv("KVSCHED_RING_WINDOW") && L_full > L_short && KV_RING_SHORT < 4096) {
+        int ps2 = 0, ps4 = 0;
+        auto kr = k_mc_ring<POL_MCSF, false>;
+        const int b2 = 4 * wbytes(L_short), b4 = 4 * wbytes(4096);
+        if ((size_t)b4 <= c->max_smem_optin) {
+            CUDA_TRY(c, cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, b4));
+            CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps2, kr, 128, b2));
+            CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps4, kr, 128, b4));
+            const long long full = (long long)ps2 * 4 * c->num_sms;
+            if ((long long)inst->n_instances < 2 * full && ps4 * 4 >= 16) {
+                L_short = L_full < 4096 ? L_full : 4096;
+                P.L = L_short;
+            }
+        }
+    }
     P.warp_bytes = wbytes(P.L);
     if ((size_t)P.warp_bytes > c->max_smem_optin)
         return fail(c, SCHED_E_ARG, "ring kernel needs %d B shared memory per warp (L=%d, NP=%d)",
