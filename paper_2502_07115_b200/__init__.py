@@ -7,9 +7,11 @@ sharding helpers (dist.py).
 """
 import os as _os
 
-# The streamed host path overlaps a persistent kernel with copy and decode work on other
-# streams; give every stream its own hardware queue (read when the CUDA context is created,
-# so this only takes effect if nothing has initialised CUDA yet; see kvsched.cu).
+# The streamed host path runs a persistent kernel that polls per-chunk flags written by a copy
+# stream's memory operations; give every stream its own hardware queue so a flag write is
+# never queued behind that kernel (read when the CUDA context is created, so this only takes
+# effect if nothing has initialised CUDA yet; a wait that gives up falls back to the chunked
+# pipeline, see kvsched.cu).
 _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 from .kvsched import (ALPHA, ALPHA_BETA, MC_BENCH, MCSF, Context, Policy, alloc_outputs, hints_of,
